@@ -1,0 +1,289 @@
+// blas.cu — launchers for the DMMA GEMM engine plus the GEMM-based triangular kernels
+// (TRSM by recursive splitting over inverted nb x nb diagonal blocks).
+//
+// Replaces cblas_ztrsm (backend.cpp:124-127), cblas_ztrmm (backend.cpp:151-155, 161-165)
+// and cblas_zgemm (backend.cpp:170-173).
+#include "blas.h"
+#include "gemm.cuh"
+
+namespace bseg {
+
+thread_local int64_t* g_launch_counter = nullptr;
+
+namespace {
+
+constexpr int kBM = 64, kBN = 64, kBK = 8, kWM = 32, kWN = 32, kST = 4;
+
+template <bool CA, bool CB>
+void launch_z(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
+  using T = ZGemmTile<kBM, kBN, kBK, kWM, kWN, kST, CA, CB>;
+  auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWN, kST, CA, CB>;
+  static bool configured = false;  // per template instance
+  if (!configured) {
+    BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(T::SMEM)));
+    configured = true;
+  }
+  kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
+  BSE_LAUNCH_CHECK();
+}
+
+void launch_z_any(cudaStream_t s, int opa, int opb, const ZGemmParams& p, dim3 grid) {
+  if (!opa && !opb) launch_z<false, false>(s, p, grid);
+  else if (!opa && opb) launch_z<false, true>(s, p, grid);
+  else if (opa && !opb) launch_z<true, false>(s, p, grid);
+  else launch_z<true, true>(s, p, grid);
+}
+
+}  // namespace
+
+__global__ void zgemm_splitk_reduce(int64_t m, int64_t n, int ksplit, const z_t* __restrict__ P,
+                                    z_t* C, int64_t ldc, z_t alpha, z_t beta, int c_lower) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    if (c_lower && i < j) continue;
+    z_t acc = P[e];
+    for (int sidx = 1; sidx < ksplit; ++sidx) acc = zadd(acc, P[int64_t(sidx) * total + e]);
+    z_t out = zmul(alpha, acc);
+    if (beta.x != 0.0 || beta.y != 0.0) out = zadd(out, zmul(beta, C[i + j * ldc]));
+    C[i + j * ldc] = out;
+  }
+}
+
+void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_t alpha,
+           const z_t* A, int64_t lda, const z_t* B, int64_t ldb, z_t beta, z_t* C, int64_t ldc,
+           int a_shape, int b_shape, int c_lower, z_t* ws, int64_t ws_elems) {
+  if (m <= 0 || n <= 0) return;
+  ZGemmParams p{};
+  p.m = m; p.n = n; p.k = k;
+  p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
+  p.alpha = alpha; p.beta = beta;
+  p.a_shape = a_shape; p.b_shape = b_shape; p.c_lower = c_lower;
+  p.ksplit = 1;
+  const int64_t tiles_m = ceil_div(m, kBM), tiles_n = ceil_div(n, kBN);
+  int ksplit = 1;
+  // Under-filled grid with a long K: split K across CTAs (deterministic two-pass reduce).
+  if (ws && tiles_m * tiles_n < 148 && k >= 8 * kBK * 4) {
+    ksplit = int(min64(ceil_div(2 * 148, tiles_m * tiles_n), k / (kBK * 16)));
+    ksplit = max(1, min(ksplit, 32));
+    while (ksplit > 1 && int64_t(ksplit) * m * n > ws_elems) --ksplit;
+  }
+  if (ksplit > 1) {
+    p.ksplit = ksplit;
+    p.P = ws;
+    launch_z_any(s, opa, opb, p, dim3(unsigned(tiles_m), unsigned(tiles_n), unsigned(ksplit)));
+    const int64_t total = m * n;
+    const int threads = 256;
+    const int blocks = int(min64(ceil_div(total, threads), 148 * 16));
+    zgemm_splitk_reduce<<<blocks, threads, 0, s>>>(m, n, ksplit, ws, C, ldc, alpha, beta,
+                                                   c_lower);
+    BSE_LAUNCH_CHECK();
+    return;
+  }
+  launch_z_any(s, opa, opb, p, dim3(unsigned(tiles_m), unsigned(tiles_n), 1));
+}
+
+void zgemm_batched(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_t alpha,
+                   const z_t* A, int64_t lda, int64_t sA, const z_t* B, int64_t ldb, int64_t sB,
+                   z_t beta, z_t* C, int64_t ldc, int64_t sC, int batch) {
+  if (m <= 0 || n <= 0 || batch <= 0) return;
+  ZGemmParams p{};
+  p.m = m; p.n = n; p.k = k;
+  p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
+  p.alpha = alpha; p.beta = beta;
+  p.sA = sA; p.sB = sB; p.sC = sC;
+  p.ksplit = 1;
+  launch_z_any(s, opa, opb, p,
+               dim3(unsigned(ceil_div(m, kBM)), unsigned(ceil_div(n, kBN)), unsigned(batch)));
+}
+
+void dgemm_nn(cudaStream_t s, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+              int batch, int64_t sA, int64_t sB, int64_t sC) {
+  if (m <= 0 || n <= 0 || batch <= 0) return;
+  constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, ST = 3;
+  using T = DGemmTile<BM, BN, BK, WM, WN, ST>;
+  auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, ST>;
+  static bool configured = false;
+  if (!configured) {
+    BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(T::SMEM)));
+    configured = true;
+  }
+  DGemmParams p{};
+  p.m = m; p.n = n; p.k = k;
+  p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
+  p.alpha = alpha; p.beta = beta;
+  p.sA = sA; p.sB = sB; p.sC = sC;
+  kern<<<dim3(unsigned(ceil_div(m, BM)), unsigned(ceil_div(n, BN)), unsigned(batch)),
+         T::NTHREADS, T::SMEM, s>>>(p);
+  BSE_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------------------
+// Inverse of each nb x nb diagonal block of a lower-triangular L (one CTA per block,
+// 4 threads per column doing strided partial dot products). Out: blocks stored
+// consecutively, each nb x nb (ld nb), strict upper zeroed.
+__global__ void __launch_bounds__(256) ztrtri_diag_kernel(int64_t n, const z_t* __restrict__ L,
+                                                          int64_t ldl, int nb, z_t* inv) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  z_t* Ls = reinterpret_cast<z_t*>(sm);      // nb x (nb+1), column-major
+  z_t* Xs = Ls + nb * (nb + 1);             // nb x (nb+1): Xs[i*(nb+1)+j] = X(i,j)
+  const int64_t b0 = int64_t(blockIdx.x) * nb;
+  const int jb = int(min64(nb, n - b0));
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    z_t v = make_double2(0.0, 0.0);
+    if (i < jb && j < jb && i >= j) v = L[(b0 + i) + (b0 + j) * ldl];
+    Ls[i + j * (nb + 1)] = v;
+    Xs[i * (nb + 1) + j] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int col = threadIdx.x >> 2, q = threadIdx.x & 3;
+  // Solve L x = e_col by forward substitution; 4 lanes share each column.
+  for (int i = 0; i < jb; ++i) {
+    z_t part = make_double2(0.0, 0.0);
+    if (col < jb && i > col) {
+      for (int kk = col + q; kk < i; kk += 4) zfma(part, Ls[i + kk * (nb + 1)], Xs[kk * (nb + 1) + col]);
+    }
+    part.x += __shfl_xor_sync(0xffffffffu, part.x, 1);
+    part.y += __shfl_xor_sync(0xffffffffu, part.y, 1);
+    part.x += __shfl_xor_sync(0xffffffffu, part.x, 2);
+    part.y += __shfl_xor_sync(0xffffffffu, part.y, 2);
+    if (col < jb && q == 0 && i >= col) {
+      const z_t lii = Ls[i + i * (nb + 1)];
+      const z_t rhs = (i == col) ? make_double2(1.0, 0.0) : make_double2(-part.x, -part.y);
+      // x_i = rhs / l_ii  (complex division; l_ii is real-positive for Cholesky factors)
+      const double den = lii.x * lii.x + lii.y * lii.y;
+      Xs[i * (nb + 1) + col] =
+          make_double2((rhs.x * lii.x + rhs.y * lii.y) / den, (rhs.y * lii.x - rhs.x * lii.y) / den);
+    }
+    __syncthreads();
+  }
+  z_t* out = inv + int64_t(blockIdx.x) * nb * nb;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    out[i + int64_t(j) * nb] = Xs[i * (nb + 1) + j];
+  }
+}
+
+void ztrtri_diag_blocks(cudaStream_t s, int64_t n, const z_t* L, int64_t ldl, int nb, z_t* inv) {
+  const int64_t nblk = ceil_div(n, nb);
+  const size_t smem = size_t(2) * nb * (nb + 1) * sizeof(z_t);
+  static bool configured = false;
+  if (!configured) {
+    BSE_CUDA(cudaFuncSetAttribute(ztrtri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+    configured = true;
+  }
+  ztrtri_diag_kernel<<<unsigned(nblk), 256, smem, s>>>(n, L, ldl, nb, inv);
+  BSE_LAUNCH_CHECK();
+}
+
+__global__ void zcopy2d_kernel(int64_t rows, int64_t cols, const z_t* __restrict__ src,
+                               int64_t lds, z_t* __restrict__ dst, int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    dst[i + j * ldd] = src[i + j * lds];
+  }
+}
+
+void zcopy2d(cudaStream_t s, int64_t rows, int64_t cols, const z_t* src, int64_t lds, z_t* dst,
+             int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return;
+  const int64_t total = rows * cols;
+  const int blocks = int(min64(ceil_div(total, 256), 148 * 32));
+  zcopy2d_kernel<<<blocks, 256, 0, s>>>(rows, cols, src, lds, dst, ldd);
+  BSE_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------------------
+// Recursive TRSM on a lower-triangular L (n x n), in place on X:
+//   side L, op N : L   X = B        side L, op C : L^H X = B
+//   side R, op N : X L   = B        side R, op C : X L^H = B
+// Leaves are nb-blocks solved as out-of-place products with the inverted diagonal block;
+// all off-diagonal work is DMMA GEMM on the largest possible panels.
+namespace {
+
+struct TrsmCtx {
+  cudaStream_t s;
+  const z_t* L;
+  int64_t ldl;
+  const z_t* inv;  // inverted diagonal blocks
+  int nb;
+  int side, op;
+  z_t* tmp;  // leaf scratch: nb x rhs_extent
+  z_t* ws;
+  int64_t ws_elems;
+};
+
+const z_t kOne = {1.0, 0.0}, kZero = {0.0, 0.0}, kMinusOne = {-1.0, 0.0};
+
+// Solve on the diagonal range [r0, r0+len) of L; X points at the full right-hand side.
+void trsm_rec(const TrsmCtx& c, int64_t r0, int64_t len, z_t* X, int64_t ldx, int64_t other) {
+  if (len <= c.nb) {
+    const z_t* Li = c.inv + (r0 / c.nb) * int64_t(c.nb) * c.nb;
+    if (c.side == 0) {
+      // X[r0:r0+len, :] = op(Linv) * X[r0:r0+len, :]
+      zgemm(c.s, c.op, 0, len, other, len, kOne, Li, c.nb, X + r0, ldx, kZero, c.tmp, len,
+            c.op ? kUpperOp : kLowerOp, kGeneral, 0, nullptr, 0);
+      zcopy2d(c.s, len, other, c.tmp, len, X + r0, ldx);
+    } else {
+      // X[:, r0:r0+len] = X[:, r0:r0+len] * op(Linv)
+      zgemm(c.s, 0, c.op, other, len, len, kOne, X + r0 * ldx, ldx, Li, c.nb, kZero, c.tmp,
+            other, kGeneral, c.op ? kUpperOp : kLowerOp, 0, nullptr, 0);
+      zcopy2d(c.s, other, len, c.tmp, other, X + r0 * ldx, ldx);
+    }
+    return;
+  }
+  const int64_t nblk = ceil_div(len, c.nb);
+  const int64_t n1 = ((nblk + 1) / 2) * c.nb;
+  const int64_t n2 = len - n1;
+  const z_t* L21 = c.L + (r0 + n1) + r0 * c.ldl;  // n2 x n1 block below the first half
+  if (c.side == 0 && c.op == 0) {
+    trsm_rec(c, r0, n1, X, ldx, other);
+    zgemm(c.s, 0, 0, n2, other, n1, kMinusOne, L21, c.ldl, X + r0, ldx, kOne, X + r0 + n1, ldx,
+          kGeneral, kGeneral, 0, c.ws, c.ws_elems);
+    trsm_rec(c, r0 + n1, n2, X, ldx, other);
+  } else if (c.side == 0 && c.op == 1) {
+    trsm_rec(c, r0 + n1, n2, X, ldx, other);
+    zgemm(c.s, 1, 0, n1, other, n2, kMinusOne, L21, c.ldl, X + r0 + n1, ldx, kOne, X + r0, ldx,
+          kGeneral, kGeneral, 0, c.ws, c.ws_elems);
+    trsm_rec(c, r0, n1, X, ldx, other);
+  } else if (c.side == 1 && c.op == 0) {
+    trsm_rec(c, r0 + n1, n2, X, ldx, other);
+    zgemm(c.s, 0, 0, other, n1, n2, kMinusOne, X + (r0 + n1) * ldx, ldx, L21, c.ldl, kOne,
+          X + r0 * ldx, ldx, kGeneral, kGeneral, 0, c.ws, c.ws_elems);
+    trsm_rec(c, r0, n1, X, ldx, other);
+  } else {
+    trsm_rec(c, r0, n1, X, ldx, other);
+    zgemm(c.s, 0, 1, other, n2, n1, kMinusOne, X + r0 * ldx, ldx, L21, c.ldl, kOne,
+          X + (r0 + n1) * ldx, ldx, kGeneral, kGeneral, 0, c.ws, c.ws_elems);
+    trsm_rec(c, r0 + n1, n2, X, ldx, other);
+  }
+}
+
+}  // namespace
+
+size_t trsm_workspace_elems(int64_t n, int64_t other, int nb) {
+  // inverted blocks + leaf scratch + split-K partials
+  return size_t(ceil_div(n, nb)) * nb * nb + size_t(nb) * size_t(other) +
+         size_t(8) * size_t(n) * size_t(nb);
+}
+
+void ztrsm_lower(cudaStream_t s, int side, int op, int64_t n, int64_t other, const z_t* L,
+                 int64_t ldl, z_t* X, int64_t ldx, z_t* ws, int nb) {
+  if (n <= 0 || other <= 0) return;
+  z_t* inv = ws;
+  z_t* tmp = inv + ceil_div(n, nb) * int64_t(nb) * nb;
+  z_t* part = tmp + int64_t(nb) * other;
+  ztrtri_diag_blocks(s, n, L, ldl, nb, inv);
+  TrsmCtx c{s, L, ldl, inv, nb, side, op, tmp, part, 8 * n * int64_t(nb)};
+  trsm_rec(c, 0, n, X, ldx, other);
+}
+
+}  // namespace bseg

@@ -1,0 +1,481 @@
+// capi.cu — the extern "C" drop-in boundary (include/bse_gpu.h).
+//
+// Every entry point maps the reference's C++ contract (proj/include/bse/backend.hpp,
+// solvers.hpp, types.hpp) onto plain pointers + status codes. Host-pointer entry points
+// stage through the context's device arena; nothing here ever computes on the CPU: when
+// no CUDA device is present every compute entry point fails with BSE_ERR_NO_DEVICE.
+#include <cfloat>
+#include <cstring>
+#include <string>
+
+#include "blas.h"
+#include "context.h"
+#include "gemm.cuh"
+#include "hetrd.h"
+#include "ops.h"
+#include "svd.h"
+
+using namespace bseg;
+
+namespace bseg {
+
+Bump arena(bse_ctx* c, size_t bytes) {
+  if (c->arena_bytes < bytes) {
+    if (c->arena) BSE_CUDA(cudaFree(c->arena));
+    c->arena = nullptr;
+    c->arena_bytes = 0;
+    const size_t want = bytes + (bytes >> 4);
+    cudaError_t e = cudaMalloc(&c->arena, want);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw CudaError(e, "workspace arena allocation");
+    }
+    c->arena_bytes = want;
+  }
+  return Bump{reinterpret_cast<char*>(c->arena), 0, c->arena_bytes};
+}
+
+}  // namespace bseg
+
+namespace {
+
+int set_status(bse_status* st, int code, const std::string& msg, int block = 0,
+               int64_t pivot = -1, double dev = 0.0) {
+  if (st) {
+    st->code = code;
+    st->block = block;
+    st->pivot_index = pivot;
+    st->relative_deviation = dev;
+    std::snprintf(st->message, sizeof(st->message), "%s", msg.c_str());
+  }
+  return code;
+}
+
+int ok(bse_status* st) { return set_status(st, BSE_OK, ""); }
+
+// Runs `fn` with the context bound (device, launch counter, lock) and maps exceptions.
+template <typename F>
+int guarded(bse_ctx* c, bse_status* st, F&& fn) {
+  if (!c) return set_status(st, BSE_ERR_INVALID_SPEC, "null context");
+  std::lock_guard<std::mutex> lock(c->mu);
+  int64_t* prev = g_launch_counter;
+  g_launch_counter = &c->launches;
+  try {
+    BSE_CUDA(cudaSetDevice(c->device));
+    fn();
+    g_launch_counter = prev;
+    return ok(st);
+  } catch (const DomainError& e) {
+    g_launch_counter = prev;
+    return set_status(st, e.code, e.msg, e.block, e.pivot);
+  } catch (const CudaError& e) {
+    g_launch_counter = prev;
+    const int code = e.err == cudaErrorMemoryAllocation ? BSE_ERR_OUT_OF_MEMORY : BSE_ERR_CUDA;
+    return set_status(st, code, e.what());
+  } catch (const std::exception& e) {
+    g_launch_counter = prev;
+    return set_status(st, BSE_ERR_GENERIC, e.what());
+  }
+}
+
+void h2d(bse_ctx* c, z_t* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+         int64_t cols) {
+  BSE_CUDA(cudaMemcpy2DAsync(dst, size_t(ldd) * sizeof(z_t), src, size_t(lds) * sizeof(z_t),
+                             size_t(rows) * sizeof(z_t), size_t(cols), cudaMemcpyHostToDevice,
+                             c->stream));
+}
+void d2h(bse_ctx* c, double* dst, int64_t ldd, const z_t* src, int64_t lds, int64_t rows,
+         int64_t cols) {
+  BSE_CUDA(cudaMemcpy2DAsync(dst, size_t(ldd) * sizeof(z_t), src, size_t(lds) * sizeof(z_t),
+                             size_t(rows) * sizeof(z_t), size_t(cols), cudaMemcpyDeviceToHost,
+                             c->stream));
+}
+
+const z_t kOne = {1.0, 0.0}, kZero = {0.0, 0.0};
+
+// Solve with device-resident buffers carved from a separate allocation (the solver pipeline
+// owns the arena). Kept simple: per-call cudaMallocAsync on the context stream.
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  DevBuf(size_t bytes, cudaStream_t st) : s(st) { BSE_CUDA(cudaMallocAsync(&p, bytes, s)); }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* as() { return reinterpret_cast<T*>(p); }
+};
+
+void run_solve(bse_ctx* c, int method, int64_t n, const z_t* A, int64_t lda, const z_t* B,
+               int64_t ldb, double* lam, z_t* V, int64_t ldv, std::vector<int64_t>& flagged) {
+  if (method == BSE_METHOD_CHOL) solve_chol_dev(c, n, A, lda, B, ldb, lam, V, ldv, flagged);
+  else if (method == BSE_METHOD_CHOL_SVD) solve_chol_svd_dev(c, n, A, lda, B, ldb, lam, V, ldv, flagged);
+  else if (method == BSE_METHOD_SQRT || method == BSE_METHOD_REFERENCE)
+    throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1,
+                      std::string("method ") + (method == BSE_METHOD_SQRT ? "sqrt" : "reference") +
+                          " is not accelerated (outside the hot-path scope)"};
+  else throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "unknown method"};
+}
+
+void check_dims(int64_t n, int64_t lda, int64_t ldb) {
+  if (n < 1) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "blocks must be at least 1x1"};
+  if (lda < n || ldb < n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "leading dimension too small"};
+}
+
+}  // namespace
+
+extern "C" {
+
+int bse_abi_version(void) { return BSE_GPU_ABI_VERSION; }
+
+int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
+  if (!out) return set_status(st, BSE_ERR_INVALID_SPEC, "null output pointer");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    (void)cudaGetLastError();
+    return set_status(st, BSE_ERR_NO_DEVICE, "no CUDA device available");
+  }
+  if (device < 0 || device >= count) return set_status(st, BSE_ERR_NO_DEVICE, "device index out of range");
+  bse_ctx* c = new bse_ctx();
+  c->device = device;
+  try {
+    BSE_CUDA(cudaSetDevice(device));
+    BSE_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& ev : c->ev) BSE_CUDA(cudaEventCreate(&ev));
+  } catch (const CudaError& ex) {
+    delete c;
+    return set_status(st, BSE_ERR_CUDA, ex.what());
+  }
+  *out = c;
+  return ok(st);
+}
+
+int bse_ctx_destroy(bse_ctx* c) {
+  if (!c) return BSE_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->arena) cudaFree(c->arena);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return BSE_OK;
+}
+
+void* bse_ctx_stream(bse_ctx* c) { return c ? reinterpret_cast<void*>(c->stream) : nullptr; }
+
+int bse_ctx_last_phase_times(bse_ctx* c, bse_phase_times* out) {
+  if (!c || !out) return BSE_ERR_INVALID_SPEC;
+  *out = c->last;
+  return BSE_OK;
+}
+
+int64_t bse_ctx_kernel_launches(bse_ctx* c) { return c ? c->launches : 0; }
+
+int bse_ctx_release_workspace(bse_ctx* c) {
+  if (!c) return BSE_OK;
+  std::lock_guard<std::mutex> lock(c->mu);
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->arena) cudaFree(c->arena);
+  c->arena = nullptr;
+  c->arena_bytes = 0;
+  return BSE_OK;
+}
+
+int bse_solve_device(bse_ctx* c, int method, int64_t n, const double* d_a, int64_t lda,
+                     const double* d_b, int64_t ldb, double* d_lambda, double* d_v, int64_t ldv,
+                     int64_t* near_singular, int64_t* n_near_singular, bse_status* st) {
+  return guarded(c, st, [&] {
+    check_dims(n, lda, ldb);
+    if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
+    std::vector<int64_t> flagged;
+    run_solve(c, method, n, reinterpret_cast<const z_t*>(d_a), lda,
+              reinterpret_cast<const z_t*>(d_b), ldb, d_lambda, reinterpret_cast<z_t*>(d_v),
+              ldv, flagged);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    if (n_near_singular) *n_near_singular = int64_t(flagged.size());
+    if (near_singular)
+      for (size_t i = 0; i < flagged.size(); ++i) near_singular[i] = flagged[i];
+  });
+}
+
+int bse_solve(bse_ctx* c, int method, int64_t n, const double* a, int64_t lda, const double* b,
+              int64_t ldb, double* lambda, double* v, int64_t ldv, int64_t* near_singular,
+              int64_t* n_near_singular, bse_status* st) {
+  return guarded(c, st, [&] {
+    check_dims(n, lda, ldb);
+    if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
+    const size_t nn = size_t(n) * size_t(n);
+    DevBuf buf(nn * 2 * sizeof(z_t) + 2 * nn * sizeof(z_t) + size_t(n) * sizeof(double) + 1024,
+               c->stream);
+    z_t* dA = buf.as<z_t>();
+    z_t* dB = dA + nn;
+    z_t* dV = dB + nn;
+    double* dL = reinterpret_cast<double*>(dV + 2 * nn);
+    h2d(c, dA, n, a, lda, n, n);
+    h2d(c, dB, n, b, ldb, n, n);
+    std::vector<int64_t> flagged;
+    run_solve(c, method, n, dA, n, dB, n, dL, dV, 2 * n, flagged);
+    BSE_CUDA(cudaMemcpyAsync(lambda, dL, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
+                             c->stream));
+    d2h(c, v, ldv, dV, 2 * n, 2 * n, n);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    if (n_near_singular) *n_near_singular = int64_t(flagged.size());
+    if (near_singular)
+      for (size_t i = 0; i < flagged.size(); ++i) near_singular[i] = flagged[i];
+  });
+}
+
+int bse_product_pair(bse_ctx* c, int64_t n, const double* a, int64_t lda, const double* b,
+                     int64_t ldb, double* m1, double* m2, bse_status* st) {
+  return guarded(c, st, [&] {
+    check_dims(n, lda, ldb);
+    const size_t nn = size_t(n) * size_t(n);
+    DevBuf buf(nn * 5 * sizeof(z_t) + 64 * 64 * sizeof(z_t) + 64, c->stream);
+    z_t* dA = buf.as<z_t>();
+    z_t* dB = dA + nn;
+    z_t* dM1 = dB + nn;
+    z_t* dM2 = dM1 + nn;
+    z_t* dW = dM2 + nn;
+    z_t* ws = dW + nn;
+    int* info = reinterpret_cast<int*>(ws + 64 * 64);
+    h2d(c, dA, n, a, lda, n, n);
+    h2d(c, dB, n, b, ldb, n, n);
+    zaddsub(c->stream, n, dA, n, dB, n, dM1, dM2, n);
+    zcopy2d(c->stream, n, n, dM1, n, dW, n);
+    zpotrf_lower(c->stream, n, dW, n, info, ws, false);
+    int h[2];
+    BSE_CUDA(cudaMemcpyAsync(&h[0], info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    zcopy2d(c->stream, n, n, dM2, n, dW, n);
+    zpotrf_lower(c->stream, n, dW, n, info, ws, false);
+    BSE_CUDA(cudaMemcpyAsync(&h[1], info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    d2h(c, m1, n, dM1, n, n, n);
+    d2h(c, m2, n, dM2, n, n, n);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    if (h[0] != 0)
+      throw DomainError{BSE_ERR_NOT_DEFINITE, BSE_BLOCK_M1, int64_t(h[0]) - 1,
+                        "A+B is not positive definite: leading minor of order " +
+                            std::to_string(h[0]) + " is not positive definite"};
+    if (h[1] != 0)
+      throw DomainError{BSE_ERR_NOT_DEFINITE, BSE_BLOCK_M2, int64_t(h[1]) - 1,
+                        "A-B is not positive definite: leading minor of order " +
+                            std::to_string(h[1]) + " is not positive definite"};
+  });
+}
+
+int bse_assemble_eigenvectors(bse_ctx* c, int64_t n, int64_t k, const double* v1, int64_t ldv1,
+                              const double* v2, int64_t ldv2, const double* lambda1,
+                              const double* lambda2, double* v, int64_t ldv, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 0 || k < 0 || ldv < 2 * n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "factor shapes do not conform"};
+    for (int64_t j = 0; j < k; ++j) {  // core.cpp:108-116 (validated on the host inputs)
+      const double x = lambda1[j], y = lambda2[j];
+      if (!(x > 0.0) || !(y > 0.0) || !std::isfinite(x) || !std::isfinite(y))
+        throw DomainError{BSE_ERR_NON_POSITIVE_SCALE, 0, -1,
+                          "scaling factor for column " + std::to_string(j) +
+                              " is not a positive finite real"};
+    }
+    if (n == 0 || k == 0) return;
+    const size_t nk = size_t(n) * size_t(k);
+    DevBuf buf(nk * 4 * sizeof(z_t) + 2 * size_t(k) * sizeof(double) + 64, c->stream);
+    z_t* d1 = buf.as<z_t>();
+    z_t* d2 = d1 + nk;
+    z_t* dV = d2 + nk;
+    double* l1 = reinterpret_cast<double*>(dV + 2 * nk);
+    double* l2 = l1 + k;
+    h2d(c, d1, n, v1, ldv1, n, k);
+    h2d(c, d2, n, v2, ldv2, n, k);
+    BSE_CUDA(cudaMemcpyAsync(l1, lambda1, sizeof(double) * size_t(k), cudaMemcpyHostToDevice, c->stream));
+    BSE_CUDA(cudaMemcpyAsync(l2, lambda2, sizeof(double) * size_t(k), cudaMemcpyHostToDevice, c->stream));
+    assemble(c->stream, n, k, d1, n, d2, n, l1, l2, 0, nullptr, l1, dV, 2 * n);
+    d2h(c, v, ldv, dV, 2 * n, 2 * n, k);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bse_cholesky_lower(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* l,
+                       int64_t ldl, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 1 || ldm < n || ldl < n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "cholesky_lower: bad dimensions"};
+    const size_t nn = size_t(n) * size_t(n);
+    DevBuf buf(nn * sizeof(z_t) + 64 * 64 * sizeof(z_t) + 64, c->stream);
+    z_t* dM = buf.as<z_t>();
+    z_t* ws = dM + nn;
+    int* info = reinterpret_cast<int*>(ws + 64 * 64);
+    h2d(c, dM, n, m, ldm, n, n);
+    zpotrf_lower(c->stream, n, dM, n, info, ws, true);
+    int h = 0;
+    BSE_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    d2h(c, l, ldl, dM, n, n, n);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    if (h > 0)
+      throw DomainError{BSE_ERR_NOT_POSITIVE_DEFINITE, 0, int64_t(h) - 1,
+                        "leading minor of order " + std::to_string(h) + " is not positive definite"};
+  });
+}
+
+int bse_matmul(bse_ctx* c, int64_t ar, int64_t ac, const double* a, int64_t lda, int op_a,
+               int shape_a, int64_t br, int64_t bc, const double* b, int64_t ldb, int op_b,
+               int shape_b, double* cmat, int64_t ldc, bse_status* st) {
+  return guarded(c, st, [&] {
+    const int64_t am = op_a == BSE_OP_NONE ? ar : ac, ak = op_a == BSE_OP_NONE ? ac : ar;
+    const int64_t bk = op_b == BSE_OP_NONE ? br : bc, bn = op_b == BSE_OP_NONE ? bc : br;
+    if (ak != bk)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1,
+                        "matmul: inner dimensions differ (" + std::to_string(am) + "x" +
+                            std::to_string(ak) + " times " + std::to_string(bk) + "x" +
+                            std::to_string(bn) + ")"};
+    const bool tri_a = shape_a != BSE_SHAPE_GENERAL, tri_b = shape_b != BSE_SHAPE_GENERAL;
+    // backend.cpp:146-167: exactly one triangular operand routes to TRMM semantics
+    int sa = kGeneral, sb = kGeneral;
+    if (tri_a && !tri_b) {
+      if (ar != ac) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "matmul (triangular operand): matrix is not square"};
+      const bool lower_op = (shape_a == BSE_SHAPE_LOWER) == (op_a == BSE_OP_NONE);
+      sa = lower_op ? kLowerOp : kUpperOp;
+    } else if (tri_b && !tri_a) {
+      if (br != bc) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "matmul (triangular operand): matrix is not square"};
+      const bool lower_op = (shape_b == BSE_SHAPE_LOWER) == (op_b == BSE_OP_NONE);
+      sb = lower_op ? kLowerOp : kUpperOp;
+    }
+    if (am == 0 || bn == 0) return;
+    const size_t na = size_t(ar) * size_t(ac), nb = size_t(br) * size_t(bc),
+                 ncm = size_t(am) * size_t(bn);
+    DevBuf buf((na + nb + ncm) * sizeof(z_t) + 64, c->stream);
+    z_t* dA = buf.as<z_t>();
+    z_t* dB = dA + na;
+    z_t* dC = dB + nb;
+    if (na) h2d(c, dA, ar, a, lda, ar, ac);
+    if (nb) h2d(c, dB, br, b, ldb, br, bc);
+    if (ak == 0) {
+      BSE_CUDA(cudaMemsetAsync(dC, 0, ncm * sizeof(z_t), c->stream));
+    } else {
+      zgemm(c->stream, op_a, op_b, am, bn, ak, kOne, dA, ar, dB, br, kZero, dC, am, sa, sb, 0,
+            nullptr, 0);
+    }
+    d2h(c, cmat, ldc, dC, am, am, bn);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bse_tri_solve(bse_ctx* c, int64_t n, const double* l, int64_t ldl, int64_t rows,
+                  int64_t cols, const double* rhs, int64_t ldr, int side, int op, double* x,
+                  int64_t ldx, bse_status* st) {
+  return guarded(c, st, [&] {
+    if ((side == BSE_SIDE_LEFT && rows != n) || (side == BSE_SIDE_RIGHT && cols != n))
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "tri_solve: right-hand side does not conform"};
+    for (int64_t i = 0; i < n; ++i) {  // backend.cpp:114-120
+      const double re = l[2 * (i + i * ldl)], im = l[2 * (i + i * ldl) + 1];
+      if (std::hypot(re, im) < DBL_MIN)
+        throw DomainError{BSE_ERR_SINGULAR_FACTOR, 0, -1,
+                          "triangular factor has a vanishing diagonal entry at index " +
+                              std::to_string(i)};
+    }
+    if (rows == 0 || cols == 0) return;
+    const size_t nn = size_t(n) * size_t(n), nr = size_t(rows) * size_t(cols);
+    const int64_t other = side == BSE_SIDE_LEFT ? cols : rows;
+    DevBuf buf((nn + nr + trsm_workspace_elems(n, other, 64)) * sizeof(z_t) + 64, c->stream);
+    z_t* dL = buf.as<z_t>();
+    z_t* dX = dL + nn;
+    z_t* ws = dX + nr;
+    h2d(c, dL, n, l, ldl, n, n);
+    h2d(c, dX, rows, rhs, ldr, rows, cols);
+    ztrsm_lower(c->stream, side == BSE_SIDE_LEFT ? 0 : 1, op == BSE_OP_NONE ? 0 : 1, n, other, dL,
+                n, dX, rows, ws, 64);
+    d2h(c, x, ldx, dX, rows, rows, cols);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bse_hermitian_eig(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* values,
+                      double* vectors, int64_t ldv, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 1 || ldm < n || ldv < n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "hermitian_eig: bad dimensions"};
+    const size_t nn = size_t(n) * size_t(n);
+    const size_t bytes = nn * 2 * sizeof(z_t) + nn * sizeof(double) + stedc_workspace_bytes(n) +
+                         hetrd_workspace_bytes(n) + unmtr_workspace_bytes(n, n) +
+                         size_t(n) * 48 + 4096;
+    Bump w = arena(c, bytes);
+    z_t* dM = w.take<z_t>(nn);
+    z_t* dZ = w.take<z_t>(nn);
+    double* Z = w.take<double>(nn);
+    void* ws_st = w.take<char>(stedc_workspace_bytes(n));
+    void* ws_ht = w.take<char>(hetrd_workspace_bytes(n));
+    void* ws_um = w.take<char>(unmtr_workspace_bytes(n, n));
+    double* d = w.take<double>(n);
+    double* e = w.take<double>(n);
+    z_t* tau = w.take<z_t>(n);
+    int* info = w.take<int>(2);
+    h2d(c, dM, n, m, ldm, n, n);
+    zhetrd_lower(c->stream, n, dM, n, d, e, tau, ws_ht);
+    dstedc(c->stream, n, d, e, Z, ws_st, info);
+    real_to_complex(c->stream, n, n, Z, n, dZ, n);
+    zunmtr_lower(c->stream, n, dM, n, tau, dZ, n, n, ws_um);
+    int h = 0;
+    BSE_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    BSE_CUDA(cudaMemcpyAsync(values, d, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, c->stream));
+    d2h(c, vectors, ldv, dZ, n, n, n);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    if (h != 0)
+      throw DomainError{BSE_ERR_CONVERGENCE_FAILURE, 0, -1,
+                        "zheevd failed to converge (info=" + std::to_string(h) + ", n=" +
+                            std::to_string(n) + ")"};
+  });
+}
+
+int bse_svd(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* u, int64_t ldu,
+            double* s, double* v, int64_t ldv, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 1 || ldm < n || ldu < n || ldv < n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "svd: bad dimensions"};
+    const size_t nn = size_t(n) * size_t(n);
+    const int64_t m2 = 2 * n;
+    const size_t bytes = nn * 5 * sizeof(z_t) + size_t(m2) * size_t(m2) * sizeof(double) +
+                         stedc_workspace_bytes(m2) + gebrd_workspace_bytes(n) +
+                         unmbr_workspace_bytes(n, n) + size_t(n) * 96 + 4096;
+    Bump w = arena(c, bytes);
+    z_t* dM = w.take<z_t>(nn);
+    z_t* dU = w.take<z_t>(nn);
+    z_t* dV = w.take<z_t>(nn);
+    z_t* dU2 = w.take<z_t>(nn);
+    z_t* dV2 = w.take<z_t>(nn);
+    double* X = w.take<double>(size_t(m2) * size_t(m2));
+    void* ws_st = w.take<char>(stedc_workspace_bytes(m2));
+    void* ws_gb = w.take<char>(gebrd_workspace_bytes(n));
+    void* ws_um = w.take<char>(unmbr_workspace_bytes(n, n));
+    double* d = w.take<double>(n);
+    double* e = w.take<double>(n);
+    double* td = w.take<double>(m2);
+    double* te = w.take<double>(m2);
+    double* sd = w.take<double>(n);
+    z_t* tq = w.take<z_t>(n);
+    z_t* tp = w.take<z_t>(n);
+    int* info = w.take<int>(2);
+    cudaStream_t sm = c->stream;
+    h2d(c, dM, n, m, ldm, n, n);
+    zgebrd_upper(sm, n, dM, n, d, e, tq, tp, ws_gb);
+    tgk_build(sm, n, d, e, td, te);
+    dstedc(sm, m2, td, te, X, ws_st, info);
+    tgk_extract(sm, n, X, dU, n, dV, n);
+    zunmbr_q(sm, n, dM, n, tq, dU, n, n, ws_um);
+    zunmbr_p(sm, n, dM, n, tp, dV, n, n, ws_um);
+    // reference convention: s descending, u/v columns to match (backend.cpp:74-84)
+    reverse_real(sm, n, td + n, sd);
+    reverse_cols(sm, n, n, dU, n, dU2, n);
+    reverse_cols(sm, n, n, dV, n, dV2, n);
+    int h = 0;
+    BSE_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, sm));
+    BSE_CUDA(cudaMemcpyAsync(s, sd, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, sm));
+    d2h(c, u, ldu, dU2, n, n, n);
+    d2h(c, v, ldv, dV2, n, n, n);
+    BSE_CUDA(cudaStreamSynchronize(sm));
+    if (h != 0) throw DomainError{BSE_ERR_CONVERGENCE_FAILURE, 0, -1, "zgesvd failed to converge"};
+  });
+}
+
+}  // extern "C"

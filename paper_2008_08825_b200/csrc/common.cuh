@@ -1,0 +1,134 @@
+// common.cuh — shared device/host helpers for the B200 (sm_100a) BSE eigensolver.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace bseg {
+
+// Interleaved complex128 (re, im) — the column-major layout of Eigen::MatrixXcd that the
+// reference uses (types.hpp:17-18); kept on device so no host-side repacking is needed.
+using z_t = double2;
+
+struct CudaError : std::runtime_error {
+  cudaError_t err;
+  CudaError(cudaError_t e, const char* what)
+      : std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e)), err(e) {}
+};
+
+#define BSE_CUDA(expr)                                              \
+  do {                                                              \
+    cudaError_t _e = (expr);                                        \
+    if (_e != cudaSuccess) throw ::bseg::CudaError(_e, #expr);      \
+  } while (0)
+
+// Every kernel launch of the library goes through this counter (bse_ctx_kernel_launches).
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch(int n = 1) {
+  if (g_launch_counter) *g_launch_counter += n;
+}
+#define BSE_LAUNCH_CHECK()                   \
+  do {                                       \
+    ::bseg::count_launch();                  \
+    BSE_CUDA(cudaGetLastError());            \
+  } while (0)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ z_t zmake(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ z_t zadd(z_t a, z_t b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ z_t zsub(z_t a, z_t b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ z_t zmul(z_t a, z_t b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+__device__ __forceinline__ z_t zcmul(z_t a, z_t b) {
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ z_t zconj(z_t a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ z_t zscale(z_t a, double s) { return make_double2(a.x * s, a.y * s); }
+// acc += a * b
+__device__ __forceinline__ void zfma(z_t& acc, z_t a, z_t b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void zcfma(z_t& acc, z_t a, z_t b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ double zabs2(z_t a) { return a.x * a.x + a.y * a.y; }
+
+// ------------------------------------------------------------------ warp/block reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ z_t warp_zsum(z_t v) {
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum; `red` must hold blockDim.x/32 doubles. Result broadcast to all threads.
+__device__ inline double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += red[w];  // fixed order: deterministic
+  return s;
+}
+
+// ------------------------------------------------------------------ async copy primitives
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 16-byte global->shared copy bypassing L1; src_bytes = 0 zero-fills (predication).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(n));
+}
+// 8-byte copy (cg only supports 16; use .ca for 8B).
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ------------------------------------------------------------------ FP64 tensor core (DMMA)
+// D(8x8) += A(8x4, row) * B(4x8, col); lane t holds A[t/4][t%4], B[t%4][t/4],
+// C[t/4][2(t%4)], C[t/4][2(t%4)+1]. Lowers to SASS DMMA.8x8x4.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+}  // namespace bseg

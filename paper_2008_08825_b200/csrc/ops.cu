@@ -1,0 +1,332 @@
+// ops.cu — bandwidth-bound glue kernels of the hot path (O(n^2) HBM traffic):
+//   product_pair's M1 = A+B, M2 = A-B          (proj/src/core.cpp:88)
+//   lambda_from_squares / clamp_singular        (proj/src/solvers.cpp:25-45, 69-88)
+//   assemble_eigenvectors + rebuild_nonpositive (proj/src/core.cpp:102-127, solvers.cpp:53-65)
+//   real D&C eigenvectors -> complex, TGK vector extraction for the SVD route.
+#include <cfloat>
+
+#include "ops.h"
+
+namespace bseg {
+
+namespace {
+inline int grid_for(int64_t total, int threads = 256) {
+  return int(min64(ceil_div(total, threads), 148 * 16));
+}
+}  // namespace
+
+__global__ void zaddsub_kernel(int64_t n, const z_t* __restrict__ A, int64_t lda,
+                               const z_t* __restrict__ B, int64_t ldb, z_t* __restrict__ M1,
+                               z_t* __restrict__ M2, int64_t ldm) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    const z_t a = A[i + j * lda], b = B[i + j * ldb];
+    if (M1) M1[i + j * ldm] = zadd(a, b);
+    if (M2) M2[i + j * ldm] = zsub(a, b);
+  }
+}
+
+void zaddsub(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* B, int64_t ldb,
+             z_t* M1, z_t* M2, int64_t ldm) {
+  zaddsub_kernel<<<grid_for(n * n), 256, 0, s>>>(n, A, lda, B, ldb, M1, M2, ldm);
+  BSE_LAUNCH_CHECK();
+}
+
+__global__ void real_to_complex_kernel(int64_t rows, int64_t cols, const double* __restrict__ Z,
+                                       int64_t ldz, z_t* __restrict__ out, int64_t ldo) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    out[i + j * ldo] = make_double2(Z[i + j * ldz], 0.0);
+  }
+}
+
+void real_to_complex(cudaStream_t s, int64_t rows, int64_t cols, const double* Z, int64_t ldz,
+                     z_t* out, int64_t ldo) {
+  real_to_complex_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, Z, ldz, out, ldo);
+  BSE_LAUNCH_CHECK();
+}
+
+// Single CTA. mode 0: lambda_from_squares(d) (d ascending, solvers.cpp:25-45);
+// mode 1: clamp_singular_ascending(s) with s ASCENDING on input (solvers.cpp:69-88; the
+// TGK route produces ascending singular values directly).
+// Outputs: lambda (n), flagged list (ascending) + count, nonpositive list + count, status
+// (0 ok, 1 = spectrum has no positive entry -> ConvergenceFailure), floor.
+__global__ void __launch_bounds__(1024) clamp_kernel(int64_t n, const double* __restrict__ d,
+                                                     int mode, double* __restrict__ lambda,
+                                                     int64_t* __restrict__ flagged,
+                                                     int64_t* __restrict__ nonpos,
+                                                     int64_t* __restrict__ counts,
+                                                     double* __restrict__ floor_out) {
+  __shared__ int64_t base_f, base_p;
+  __shared__ int wf[32], wp[32];
+  const double dmax = d[n - 1];
+  if (!(dmax > 0.0)) {
+    if (threadIdx.x == 0) {
+      counts[0] = 0;
+      counts[1] = 0;
+      counts[2] = 1;
+    }
+    return;
+  }
+  const double fl = mode == 0 ? DBL_EPSILON * sqrt(dmax) : DBL_EPSILON * dmax;
+  if (threadIdx.x == 0) {
+    base_f = 0;
+    base_p = 0;
+    *floor_out = fl;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int64_t i = c0 + threadIdx.x;
+    bool f = false, p = false;
+    if (i < n) {
+      const double di = d[i];
+      double lam;
+      if (mode == 0) {
+        lam = di > 0.0 ? sqrt(di) : 0.0;
+        p = !(di > 0.0);
+      } else {
+        lam = di;
+      }
+      if (lam < fl) {
+        lam = fl;
+        f = true;
+      } else {
+        p = false;
+      }
+      if (!f) p = false;
+      lambda[i] = lam;
+    }
+    const unsigned bf = __ballot_sync(0xffffffffu, f), bp = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) {
+      wf[wid] = __popc(bf);
+      wp[wid] = __popc(bp);
+    }
+    __syncthreads();
+    int64_t of = base_f, op = base_p;
+    for (int w = 0; w < wid; ++w) {
+      of += wf[w];
+      op += wp[w];
+    }
+    const unsigned lm = (1u << lane) - 1u;
+    if (f) flagged[of + __popc(bf & lm)] = i;
+    if (p) nonpos[op + __popc(bp & lm)] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 0; w < nw; ++w) {
+        base_f += wf[w];
+        base_p += wp[w];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = base_f;
+    counts[1] = base_p;
+    counts[2] = 0;
+  }
+}
+
+void clamp_spectrum(cudaStream_t s, int64_t n, const double* d, int mode, double* lambda,
+                    int64_t* flagged, int64_t* nonpos, int64_t* counts, double* floor_out) {
+  clamp_kernel<<<1, 1024, 0, s>>>(n, d, mode, lambda, flagged, nonpos, counts, floor_out);
+  BSE_LAUNCH_CHECK();
+}
+
+// assemble_eigenvectors (core.cpp:102-127) with per-column factors (lambda1, lambda2):
+//   x = v1 * (l1/l2)^(1/4), y = v2 * (l2/l1)^(1/4), V = [(x+y)/2 ; (y-x)/2]
+// and the breakdown rebuild (solvers.cpp:53-65) for columns whose squared eigenvalue d_j
+// came out nonpositive (nonpos_mask: d != nullptr and d[j] <= 0): q = sqrt(mag) e^{i pi/4}
+// with mag = max(sqrt|d_j|, floor), x = v1 q, y = v2 / q.
+__global__ void assemble_kernel(int64_t n, int64_t k, const z_t* __restrict__ V1, int64_t ld1,
+                                const z_t* __restrict__ V2, int64_t ld2,
+                                const double* __restrict__ l1, const double* __restrict__ l2,
+                                int l2_is_one, const double* __restrict__ dsq,
+                                const double* __restrict__ floor_p, z_t* __restrict__ V,
+                                int64_t ldv) {
+  const int64_t total = n * k;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    const z_t a = V1[i + j * ld1], b = V2[i + j * ld2];
+    z_t x, y;
+    if (dsq && !(dsq[j] > 0.0)) {
+      const double mag = fmax(sqrt(fabs(dsq[j])), *floor_p);
+      const double r = sqrt(mag) * 0.70710678118654752440;
+      const z_t q = make_double2(r, r);
+      x = zmul(a, q);
+      // b / q
+      const double den = q.x * q.x + q.y * q.y;
+      y = make_double2((b.x * q.x + b.y * q.y) / den, (b.y * q.x - b.x * q.y) / den);
+    } else {
+      const double lam1 = l1[j], lam2 = l2_is_one ? 1.0 : l2[j];
+      const double s1 = pow(lam1 / lam2, 0.25), s2 = pow(lam2 / lam1, 0.25);
+      x = zscale(a, s1);
+      y = zscale(b, s2);
+    }
+    V[i + j * ldv] = zscale(zadd(x, y), 0.5);
+    V[(n + i) + j * ldv] = zscale(zsub(y, x), 0.5);
+  }
+}
+
+void assemble(cudaStream_t s, int64_t n, int64_t k, const z_t* V1, int64_t ld1, const z_t* V2,
+              int64_t ld2, const double* l1, const double* l2, int l2_is_one, const double* dsq,
+              const double* floor_p, z_t* V, int64_t ldv) {
+  assemble_kernel<<<grid_for(n * k), 256, 0, s>>>(n, k, V1, ld1, V2, ld2, l1, l2, l2_is_one, dsq,
+                                                  floor_p, V, ldv);
+  BSE_LAUNCH_CHECK();
+}
+
+// Validates the assemble_eigenvectors scale factors (NonPositiveScale, core.cpp:108-116).
+__global__ void check_scales_kernel(int64_t k, const double* l1, const double* l2, int* bad) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < k;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const double a = l1[j], b = l2[j];
+    if (!(a > 0.0) || !(b > 0.0) || !isfinite(a) || !isfinite(b)) atomicMin(bad, int(j));
+  }
+}
+
+void check_scales(cudaStream_t s, int64_t k, const double* l1, const double* l2, int* bad) {
+  check_scales_kernel<<<grid_for(k), 256, 0, s>>>(k, l1, l2, bad);
+  BSE_LAUNCH_CHECK();
+}
+
+// TGK route: eigenvectors X (2n x 2n real, ld 2n, ascending eigenvalues) of the Golub–Kahan
+// tridiagonal with off-diagonal (d1, e1, d2, e2, ...). The top n columns (positive
+// eigenvalues sigma ascending) hold x = [v1, u1, v2, u2, ...]/sqrt(2) interleaved.
+// Outputs complex Ub = sqrt(2) x_odd, Vb = sqrt(2) x_even for column j (sigma_j ascending),
+// each re-normalised separately (removes the +sigma/-sigma mixing for tiny sigma).
+__global__ void tgk_extract_kernel(int64_t n, const double* __restrict__ X,
+                                   z_t* __restrict__ Ub, int64_t ldu, z_t* __restrict__ Vb,
+                                   int64_t ldv) {
+  const int64_t j = blockIdx.x;  // one CTA per singular vector pair
+  const double* x = X + (n + j) * (2 * n);
+  __shared__ double red[32];
+  double su = 0.0, sv = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double a = x[2 * i], b = x[2 * i + 1];
+    sv += a * a;
+    su += b * b;
+  }
+  su = block_sum(su, red);
+  sv = block_sum(sv, red);
+  const double ru = su > 0.0 ? 1.0 / sqrt(su) : 0.0, rv = sv > 0.0 ? 1.0 / sqrt(sv) : 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    Vb[i + j * ldv] = make_double2(x[2 * i] * rv, 0.0);
+    Ub[i + j * ldu] = make_double2(x[2 * i + 1] * ru, 0.0);
+  }
+}
+
+void tgk_extract(cudaStream_t s, int64_t n, const double* X, z_t* Ub, int64_t ldu, z_t* Vb,
+                 int64_t ldv) {
+  tgk_extract_kernel<<<unsigned(n), 256, 0, s>>>(n, X, Ub, ldu, Vb, ldv);
+  BSE_LAUNCH_CHECK();
+}
+
+// TGK tridiagonal: diag 0, off-diagonal interleaving d (n) and e (n-1).
+__global__ void tgk_build_kernel(int64_t n, const double* __restrict__ d,
+                                 const double* __restrict__ e, double* __restrict__ td,
+                                 double* __restrict__ te) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < 2 * n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    td[i] = 0.0;
+    if (i < 2 * n - 1) te[i] = (i % 2 == 0) ? d[i / 2] : e[i / 2];
+  }
+}
+
+void tgk_build(cudaStream_t s, int64_t n, const double* d, const double* e, double* td,
+               double* te) {
+  tgk_build_kernel<<<grid_for(2 * n), 256, 0, s>>>(n, d, e, td, te);
+  BSE_LAUNCH_CHECK();
+}
+
+// Right-scale columns by r_j = 1/sqrt(lambda_j) (CHOL+SVD, solvers.cpp:152-156).
+__global__ void scale_cols_rsqrt_kernel(int64_t rows, int64_t cols, z_t* __restrict__ X,
+                                        int64_t ldx, const double* __restrict__ lam) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    X[i + j * ldx] = zscale(X[i + j * ldx], 1.0 / sqrt(lam[j]));
+  }
+}
+
+void scale_cols_rsqrt(cudaStream_t s, int64_t rows, int64_t cols, z_t* X, int64_t ldx,
+                      const double* lam) {
+  scale_cols_rsqrt_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, X, ldx, lam);
+  BSE_LAUNCH_CHECK();
+}
+
+__global__ void square_vec_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    b[i] = a[i] * a[i];
+}
+
+void square_vec(cudaStream_t s, int64_t n, const double* a, double* b) {
+  square_vec_kernel<<<grid_for(n), 256, 0, s>>>(n, a, b);
+  BSE_LAUNCH_CHECK();
+}
+
+__global__ void reverse_real_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    b[i] = a[n - 1 - i];
+}
+
+void reverse_real(cudaStream_t s, int64_t n, const double* a, double* b) {
+  reverse_real_kernel<<<grid_for(n), 256, 0, s>>>(n, a, b);
+  BSE_LAUNCH_CHECK();
+}
+
+// Column reversal of a complex matrix (svd's descending convention <-> ascending).
+__global__ void reverse_cols_kernel(int64_t rows, int64_t cols, const z_t* __restrict__ a,
+                                    int64_t lda, z_t* __restrict__ b, int64_t ldb) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    b[i + j * ldb] = a[i + (cols - 1 - j) * lda];
+  }
+}
+
+void reverse_cols(cudaStream_t s, int64_t rows, int64_t cols, const z_t* a, int64_t lda, z_t* b,
+                  int64_t ldb) {
+  reverse_cols_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, a, lda, b, ldb);
+  BSE_LAUNCH_CHECK();
+}
+
+// Hermitian deviation check & symmetrisation of from_blocks (core.cpp:45-57): partial sums
+// of |m|^2 and |m - m^H|^2 per CTA (deterministic second pass on host).
+__global__ void herm_dev_kernel(int64_t n, const z_t* __restrict__ M, int64_t ld,
+                                double* __restrict__ part) {
+  __shared__ double red[32];
+  double nrm = 0.0, dev = 0.0;
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    const z_t a = M[i + j * ld], b = M[j + i * ld];
+    nrm += zabs2(a);
+    const z_t d = make_double2(a.x - b.x, a.y + b.y);
+    dev += zabs2(d);
+  }
+  nrm = block_sum(nrm, red);
+  dev = block_sum(dev, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = nrm;
+    part[2 * blockIdx.x + 1] = dev;
+  }
+}
+
+void herm_dev_partials(cudaStream_t s, int64_t n, const z_t* M, int64_t ld, double* part,
+                       int nblocks) {
+  herm_dev_kernel<<<nblocks, 256, 0, s>>>(n, M, ld, part);
+  BSE_LAUNCH_CHECK();
+}
+
+}  // namespace bseg
