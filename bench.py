@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py — BSE eigensolve throughput on B200 (BASELINE.json metric, config 5).
+
+Workload (config 5): a batch of 64 independent complex128 n=4096 BSE matrices (config-2
+generator, seeds 0..63), CHOL method, partitioned across ranks by seed (rank r solves seeds
+r, r+N, ...). One "step" = every rank solves one matrix of its shard (inputs resident in
+HBM, distinct seed per step); NCCL only gathers the per-matrix eigenvalues to all ranks.
+value = whole-job FP64 TFLOP/s under the reference flop model (160/3 n^3 real flops per
+complex CHOL solve, proj/src/bench.cpp:41-50 x4 for complex).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 4096]
+                  [--method chol|chol-svd] [--no-cpu-baseline]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+FLOP_COEFF = {"chol": 160.0 / 3.0, "chol-svd": 296.0 / 3.0}  # Table 1 x4 complex
+
+
+def flops(method: str, n: int) -> float:
+    return FLOP_COEFF[method] * float(n) ** 3
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, v in zip(names, s[3:7]):
+                if v.lower() == "active":
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def seeds_for(rank: int, world: int, steps: int, offset: int = 0):
+    """Seed partition of the 64-matrix batch: rank r owns r, r+N, ...; step k -> k-th own seed."""
+    own = [s for s in range(64) if s % world == rank]
+    return [own[(offset + k) % len(own)] for k in range(steps)]
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (LAPACK restatement, oracle/) on the host."""
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2008_08825_b200 import configs
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    method = args.method
+    n = args.n
+    # warm-up steps: small instances page in OpenBLAS and its thread pool
+    a, b = configs.config5(0, n=256)
+    for _ in range(args.warmup):
+        oracle.solve(method, a, b)
+    times = []
+    for k in range(args.steps):
+        a, b = configs.config5(k % 64, n=n)
+        t0 = time.perf_counter()
+        oracle.solve(method, a, b)
+        times.append(time.perf_counter() - t0)
+    t = sum(times)
+    value = flops(method, n) * args.steps / t / 1e12
+    line = {
+        "impl": "reference",
+        "metric": f"BSE eigensolve FP64 TFLOP/s (Table-1 flop model), n={n} c128, {method}",
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"config5: batch of 64 complex128 n={n} BSE matrices, {method}; "
+                               "reference arm = 1 matrix per step on the host CPU",
+                   "n": n, "method": method, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full {method} solve(s) of config-5 matrices "
+                                   f"n={n} (oracle/ LAPACK restatement, OpenBLAS "
+                                   f"{oracle.blas_config().split()[1]})"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "s_per_solve": t / args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--method", default="chol", choices=["chol", "chol-svd"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    import paper_2008_08825_b200 as bse
+    from paper_2008_08825_b200 import configs
+    dev = torch.device("cuda", local)
+    n, method = args.n, args.method
+    meth = bse.Method.Chol if method == "chol" else bse.Method.CholSvd
+    ctx = bse.Context(local)
+    ctx.set_kernel_timing(True)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+
+    # ---- inputs: W + K distinct matrices of this rank's shard, resident in HBM
+    total = args.warmup + args.steps
+    seeds = seeds_for(rank, world, total)
+    host = []
+    d_in = []
+    for sd in seeds:
+        a, b = configs.config5(sd, n=n)
+        ha = torch.from_numpy(a.T).pin_memory()  # same bytes, column-major complex128
+        hb = torch.from_numpy(b.T).pin_memory()
+        host.append((ha, hb))
+        d_in.append((ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)))
+    torch.cuda.synchronize()
+    d_lam = torch.empty(n, dtype=torch.float64, device=dev)
+    d_v = torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)  # 2n x n column-major
+    lam_all = torch.empty((world, n), dtype=torch.float64, device=dev)
+
+    def step(i):
+        da, db = d_in[i]
+        bse.solve_device(meth, n, da.data_ptr(), db.data_ptr(), d_lam.data_ptr(), d_v.data_ptr(),
+                         ctx=ctx)
+        if world > 1:
+            import torch.distributed as dist
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(lam_all, d_lam)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    launches0 = ctx.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    phase_hist = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+            phase_hist.append(ctx.phase_times())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.kernel_launches() - launches0
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * flops(method, n) / (ms_per_step / 1e3) / 1e12
+
+    # ---- end to end through the host-pointer C-ABI (bse_solve): H2D + solve + D2H per step
+    e2e = None
+    if not args.no_e2e:
+        hv = torch.empty((n, 2 * n), dtype=torch.complex128).pin_memory()
+        hl = torch.empty(n, dtype=torch.float64).pin_memory()
+        import ctypes
+        L = bse._lib.lib()
+        st = bse.Status()
+        ns = np.zeros(n, dtype=np.int64)
+        nn = ctypes.c_int64(0)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            ha, hb = host[args.warmup + k]
+            rc = L.bse_solve(ctx.handle, int(meth), n, ctypes.c_void_p(ha.data_ptr()), n,
+                             ctypes.c_void_p(hb.data_ptr()), n, ctypes.c_void_p(hl.data_ptr()),
+                             ctypes.c_void_p(hv.data_ptr()), 2 * n,
+                             ns.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nn), ctypes.byref(st))
+            if rc != 0:
+                raise RuntimeError(st.message.decode())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * flops(method, n) / (ems / args.steps / 1e3) / 1e12,
+               "unit": "TFLOP/s", "h2d_bytes_per_step": 2 * n * n * 16,
+               "d2h_bytes_per_step": 2 * n * n * 16 + n * 8,
+               "ms_per_step": ems / args.steps, "path": "bse_solve (host pointers, pinned)"}
+
+    # ---- roofline of the dominant kernel class from the live event timings
+    peaks = load_peaks()
+    ph = phase_hist[-1]
+    panel = {"ms": ph["panel_ms"], "launches": ph["panel_launches"], "bytes": ph["panel_bytes"]}
+    gemm = {"ms": ph["gemm_ms"], "launches": ph["gemm_launches"], "flops": ph["gemm_flops"]}
+    fp64_peak = 37.0  # DMMA m8n8k4 issue-rate probe on this pool (tools/microbench/fp64_peak.cu)
+    if panel["ms"] >= gemm["ms"]:
+        ach = panel["bytes"] / (panel["ms"] / 1e3) / 1e9
+        pk = peaks.get("hbm_gbs", 6650.0)
+        roofline = {"bound": "hbm", "kernel": "hetrd/gebrd cooperative panel kernel",
+                    "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk,
+                    "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                    "per_launch_ms": panel["ms"] / max(panel["launches"], 1),
+                    "algorithmic_bytes_per_launch": panel["bytes"] / max(panel["launches"], 1)}
+    else:
+        ach = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12
+        roofline = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (DMMA.8x8x4)",
+                    "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                    "traffic": None,
+                    "peak_source": "measured FP64 DMMA probe (MEASURED_PEAKS.json has no FP64)",
+                    "per_launch_ms": gemm["ms"] / max(gemm["launches"], 1)}
+    try:
+        with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        roofline["traffic"] = tr.get(roofline["bound"])
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        cores = os.cpu_count() or 1
+        oracle.set_threads(cores)
+        a, b = configs.config5(seeds[args.warmup], n=n)
+        t0 = time.perf_counter()
+        oracle.solve(method, a, b)
+        tc = time.perf_counter() - t0
+        cpu = {"value": flops(method, n) / tc / 1e12, "unit": "TFLOP/s", "cores": cores,
+               "kind": "port", "s_per_solve": tc,
+               "sample": f"one {method} solve of config-5 seed {seeds[args.warmup]} (n={n}) with "
+                         f"the oracle/ LAPACK restatement on {cores} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": f"BSE eigensolve FP64 TFLOP/s (Table-1 flop model), n={n} c128, {method}",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": f"config5: batch of 64 complex128 n={n} BSE matrices "
+                                   f"(config-2 generator, seeds 0..63), {method}; each step every "
+                                   "GPU solves one matrix of its seed shard",
+                       "n": n, "method": method, "batch": 64, "matrices_per_step_per_gpu": 1,
+                       "l2": "inputs 512 MiB per solve (> 126 MB L2), distinct per step",
+                       "parallelism": f"dp{world} (seed partition, NCCL gathers eigenvalues)"},
+            "s_per_solve": ms_per_step / 1e3,
+            "batch64_s": ms_per_step / 1e3 * 64 / world,
+            "fp64_frac_of_peak": value / (world * fp64_peak),
+            "phase_ms": {k: round(v, 3) for k, v in ph.items()
+                         if k in ("product_pair", "triple", "reduce", "tridiag", "backtransform",
+                                  "recover", "total")},
+            "kernels": {"panel": panel, "gemm": gemm,
+                        "gemm_tflops": gemm["flops"] / max(gemm["ms"], 1e-9) / 1e9},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -78,6 +78,13 @@ typedef struct bse_phase_times {
   double backtransform; /* unmtr / unmbr                                                  */
   double recover;       /* TRSM/TRMM + scaling + assembly                                 */
   double total;
+  /* Live per-kernel timing (CUDA events on the context stream around each launch):      */
+  double panel_ms;      /* sum over the reduction panel kernels (hetrd / gebrd)           */
+  double panel_launches;
+  double panel_bytes;   /* algorithmic HBM bytes those launches must stream               */
+  double gemm_ms;       /* sum over DMMA GEMM launches of the solve                        */
+  double gemm_launches;
+  double gemm_flops;    /* executed real flops of those GEMM launches                      */
 } bse_phase_times;
 
 /* ---------------------------------------------------------------- context */
@@ -92,6 +99,8 @@ void* bse_ctx_stream(bse_ctx* ctx);
 int bse_ctx_last_phase_times(bse_ctx* ctx, bse_phase_times* out);
 /* Number of kernels this library launched on the context since creation. */
 int64_t bse_ctx_kernel_launches(bse_ctx* ctx);
+/* Enables CUDA-event timing of the panel and GEMM kernels (fills panel_ and gemm_ fields). */
+int bse_ctx_set_kernel_timing(bse_ctx* ctx, int enable);
 /* Frees the cached workspace arena (it is otherwise reused across calls). */
 int bse_ctx_release_workspace(bse_ctx* ctx);
 int bse_abi_version(void);

@@ -237,6 +237,9 @@ class Context:
         _lib.lib().bse_ctx_last_phase_times(self._h, ctypes.byref(t))
         return {k: getattr(t, k) for k, _ in PhaseTimes._fields_}
 
+    def set_kernel_timing(self, enable: bool = True):
+        _lib.lib().bse_ctx_set_kernel_timing(self._h, 1 if enable else 0)
+
     def kernel_launches(self) -> int:
         return int(_lib.lib().bse_ctx_kernel_launches(self._h))
 

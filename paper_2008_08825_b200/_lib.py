@@ -31,7 +31,8 @@ class Status(ctypes.Structure):
 class PhaseTimes(ctypes.Structure):
     _fields_ = [(k, ctypes.c_double) for k in (
         "product_pair", "cholesky", "triple", "reduce", "tridiag", "backtransform", "recover",
-        "total")]
+        "total", "panel_ms", "panel_launches", "panel_bytes", "gemm_ms", "gemm_launches",
+        "gemm_flops")]
 
 
 # (name, restype, argtypes) for every symbol include/bse_gpu.h declares.
@@ -43,6 +44,7 @@ SYMBOLS = {
     "bse_ctx_last_phase_times": (c_int, [c_dp, ctypes.POINTER(PhaseTimes)]),
     "bse_ctx_kernel_launches": (c_i64, [c_dp]),
     "bse_ctx_release_workspace": (c_int, [c_dp]),
+    "bse_ctx_set_kernel_timing": (c_int, [c_dp, c_int]),
     "bse_solve": (c_int, [c_dp, c_int, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_dp, c_i64, c_dp,
                           c_dp, ctypes.POINTER(Status)]),
     "bse_solve_device": (c_int, [c_dp, c_int, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_dp, c_i64,

@@ -9,6 +9,7 @@
 namespace bseg {
 
 thread_local int64_t* g_launch_counter = nullptr;
+thread_local KernelTimer* g_timer = nullptr;
 
 namespace {
 
@@ -52,10 +53,36 @@ __global__ void zgemm_splitk_reduce(int64_t m, int64_t n, int ksplit, const z_t*
   }
 }
 
+namespace {
+// Executed real flops of one zgemm call (8 per complex MAC) with triangular K skipping and
+// skipped upper tiles, counted per 64x64 tile exactly as the kernel bounds its K loop.
+double zgemm_exec_flops(int64_t m, int64_t n, int64_t k, int a_shape, int b_shape, int c_lower) {
+  double f = 0.0;
+  for (int64_t m0 = 0; m0 < m; m0 += kBM)
+    for (int64_t n0 = 0; n0 < n; n0 += kBN) {
+      if (c_lower && m0 + kBM <= n0) continue;
+      int64_t lo = 0, hi = k;
+      if (a_shape == kLowerOp) hi = min64(hi, m0 + kBM);
+      if (a_shape == kUpperOp) lo = max64(lo, m0);
+      if (b_shape == kLowerOp) lo = max64(lo, n0);
+      if (b_shape == kUpperOp) hi = min64(hi, n0 + kBN);
+      if (hi > lo) f += 8.0 * double(min64(kBM, m - m0)) * double(min64(kBN, n - n0)) * double(hi - lo);
+    }
+  return f;
+}
+}  // namespace
+
 void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_t alpha,
            const z_t* A, int64_t lda, const z_t* B, int64_t ldb, z_t beta, z_t* C, int64_t ldc,
            int a_shape, int b_shape, int c_lower, z_t* ws, int64_t ws_elems) {
   if (m <= 0 || n <= 0) return;
+  const int slot =
+      g_timer ? timer_begin(s, 0, zgemm_exec_flops(m, n, k, a_shape, b_shape, c_lower)) : -1;
+  struct End {
+    cudaStream_t s;
+    int slot;
+    ~End() { timer_end(s, slot); }
+  } end_guard{s, slot};
   ZGemmParams p{};
   p.m = m; p.n = n; p.k = k;
   p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;

@@ -59,22 +59,55 @@ int guarded(bse_ctx* c, bse_status* st, F&& fn) {
   if (!c) return set_status(st, BSE_ERR_INVALID_SPEC, "null context");
   std::lock_guard<std::mutex> lock(c->mu);
   int64_t* prev = g_launch_counter;
+  KernelTimer* prev_timer = g_timer;
   g_launch_counter = &c->launches;
+  if (c->timing) {
+    c->timer.pool = c->timer_events.data();
+    c->timer.capacity = int(c->timer_events.size());
+    c->timer.used = 0;
+    g_timer = &c->timer;
+  }
+  struct Restore {
+    int64_t* a;
+    KernelTimer* b;
+    ~Restore() {
+      g_launch_counter = a;
+      g_timer = b;
+    }
+  } restore{prev, prev_timer};
   try {
     BSE_CUDA(cudaSetDevice(c->device));
     fn();
-    g_launch_counter = prev;
     return ok(st);
   } catch (const DomainError& e) {
-    g_launch_counter = prev;
     return set_status(st, e.code, e.msg, e.block, e.pivot);
   } catch (const CudaError& e) {
-    g_launch_counter = prev;
     const int code = e.err == cudaErrorMemoryAllocation ? BSE_ERR_OUT_OF_MEMORY : BSE_ERR_CUDA;
     return set_status(st, code, e.what());
   } catch (const std::exception& e) {
-    g_launch_counter = prev;
     return set_status(st, BSE_ERR_GENERIC, e.what());
+  }
+}
+
+// Sums the timed launches of the last solve into c->last (after a stream sync).
+void collect_timer(bse_ctx* c) {
+  if (!c->timing) return;
+  BSE_CUDA(cudaStreamSynchronize(c->stream));
+  bse_phase_times& t = c->last;
+  t.panel_ms = t.gemm_ms = t.panel_bytes = t.gemm_flops = 0.0;
+  t.panel_launches = t.gemm_launches = 0.0;
+  for (int i = 0; i < c->timer.used / 2; ++i) {
+    float ms = 0.f;
+    BSE_CUDA(cudaEventElapsedTime(&ms, c->timer.pool[2 * i], c->timer.pool[2 * i + 1]));
+    if (c->timer.kind[i] == 0) {
+      t.gemm_ms += ms;
+      t.gemm_flops += c->timer.work[i];
+      t.gemm_launches += 1;
+    } else {
+      t.panel_ms += ms;
+      t.panel_bytes += c->timer.work[i];
+      t.panel_launches += 1;
+    }
   }
 }
 
@@ -157,6 +190,7 @@ int bse_ctx_destroy(bse_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->arena) cudaFree(c->arena);
+  for (auto& ev : c->timer_events) cudaEventDestroy(ev);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -173,6 +207,19 @@ int bse_ctx_last_phase_times(bse_ctx* c, bse_phase_times* out) {
 }
 
 int64_t bse_ctx_kernel_launches(bse_ctx* c) { return c ? c->launches : 0; }
+
+int bse_ctx_set_kernel_timing(bse_ctx* c, int enable) {
+  if (!c) return BSE_ERR_INVALID_SPEC;
+  std::lock_guard<std::mutex> lock(c->mu);
+  cudaSetDevice(c->device);
+  c->timing = enable != 0;
+  if (c->timing && c->timer_events.empty()) {
+    c->timer_events.resize(8192);
+    for (auto& e : c->timer_events)
+      if (cudaEventCreate(&e) != cudaSuccess) return BSE_ERR_CUDA;
+  }
+  return BSE_OK;
+}
 
 int bse_ctx_release_workspace(bse_ctx* c) {
   if (!c) return BSE_OK;
@@ -196,6 +243,7 @@ int bse_solve_device(bse_ctx* c, int method, int64_t n, const double* d_a, int64
               reinterpret_cast<const z_t*>(d_b), ldb, d_lambda, reinterpret_cast<z_t*>(d_v),
               ldv, flagged);
     BSE_CUDA(cudaStreamSynchronize(c->stream));
+    collect_timer(c);
     if (n_near_singular) *n_near_singular = int64_t(flagged.size());
     if (near_singular)
       for (size_t i = 0; i < flagged.size(); ++i) near_singular[i] = flagged[i];
@@ -219,6 +267,7 @@ int bse_solve(bse_ctx* c, int method, int64_t n, const double* a, int64_t lda, c
     h2d(c, dB, n, b, ldb, n, n);
     std::vector<int64_t> flagged;
     run_solve(c, method, n, dA, n, dB, n, dL, dV, 2 * n, flagged);
+    collect_timer(c);
     BSE_CUDA(cudaMemcpyAsync(lambda, dL, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
                              c->stream));
     d2h(c, v, ldv, dV, 2 * n, 2 * n, n);

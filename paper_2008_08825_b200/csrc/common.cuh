@@ -38,6 +38,31 @@ inline void count_launch(int n = 1) {
     BSE_CUDA(cudaGetLastError());            \
   } while (0)
 
+// Optional live per-kernel timing (enabled per context): CUDA event pairs around the
+// dominant kernel classes, summed after the solve. kind 0 = DMMA GEMM, 1 = panel kernel.
+struct KernelTimer {
+  cudaEvent_t* pool = nullptr;
+  int capacity = 0;
+  int used = 0;
+  int kind[4096];
+  double work[4096];  // flops (GEMM) or algorithmic bytes (panel) of each timed launch
+};
+extern thread_local KernelTimer* g_timer;
+inline int timer_begin(cudaStream_t s, int kind, double work) {
+  KernelTimer* t = g_timer;
+  if (!t || t->used + 2 > t->capacity || t->used / 2 >= 4096) return -1;
+  const int slot = t->used / 2;
+  t->kind[slot] = kind;
+  t->work[slot] = work;
+  cudaEventRecord(t->pool[t->used], s);
+  t->used += 2;
+  return slot;
+}
+inline void timer_end(cudaStream_t s, int slot) {
+  if (slot < 0 || !g_timer) return;
+  cudaEventRecord(g_timer->pool[2 * slot + 1], s);
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -16,6 +16,10 @@ struct bse_ctx {
   bse_phase_times last{};
   cudaEvent_t ev[12]{};
   std::mutex mu;
+  // live per-kernel timing (bse_ctx_set_kernel_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> timer_events;
+  bseg::KernelTimer timer;
 };
 
 namespace bseg {

@@ -411,8 +411,15 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     int G = int(min64(int64_t(blocks_per_sm) * num_sms, max64(tiles, ceil_div(m, kRB))));
     G = max(G, 1);
     void* args[] = {&a};
+    double bytes = 0.0;  // algorithmic: A^H v over (n-g) x (n-g-1) and A u over (n-g-1)^2
+    for (int i = 0; i < nbp; ++i) {
+      const double r = double(n - (p0 + i));
+      bytes += (r * (r - 1.0) + (r - 1.0) * (r - 1.0)) * sizeof(z_t);
+    }
+    const int slot = g_timer ? timer_begin(s, 1, bytes) : -1;
     BSE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(gebrd_panel_kernel), dim3(G),
                                          dim3(kThreads), args, smem, s));
+    timer_end(s, slot);
     count_launch();
     const int64_t q = p0 + nbp;
     if (q < n) {

@@ -390,8 +390,15 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     int G = int(min64(int64_t(blocks_per_sm) * num_sms, max64(tiles, ceil_div(m, kRB))));
     G = max(G, 1);
     void* args[] = {&a};
+    double bytes = 0.0;  // algorithmic: lower triangle of each column's trailing matrix
+    for (int i = 0; i < nbp; ++i) {
+      const double mt = double(n - (p0 + i) - 1);
+      bytes += 0.5 * mt * (mt + 1.0) * sizeof(z_t);
+    }
+    const int slot = g_timer ? timer_begin(s, 1, bytes) : -1;
     BSE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(hetrd_panel_kernel), dim3(G),
                                          dim3(kThreads), args, smem, s));
+    timer_end(s, slot);
     count_launch();
     const int64_t q = p0 + nbp;
     if (q < n) {
