@@ -500,7 +500,7 @@ int bse_svd(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* u, int6
     double* d = w.take<double>(n);
     double* e = w.take<double>(n);
     double* td = w.take<double>(m2);
-    double* te = w.take<double>(m2);
+    double* te = w.take<double>(m2 + 8);
     double* sd = w.take<double>(n);
     z_t* tq = w.take<z_t>(n);
     z_t* tp = w.take<z_t>(n);
@@ -514,6 +514,7 @@ int bse_svd(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* u, int6
     zunmbr_q(sm, n, dM, n, tq, dU, n, n, ws_um);
     zunmbr_p(sm, n, dM, n, tp, dV, n, n, ws_um);
     // reference convention: s descending, u/v columns to match (backend.cpp:74-84)
+    tgk_refine(sm, n, d, e, td + n, te);  // relative accuracy, as zbdsqr
     reverse_real(sm, n, td + n, sd);
     reverse_cols(sm, n, n, dU, n, dU2, n);
     reverse_cols(sm, n, n, dV, n, dV2, n);

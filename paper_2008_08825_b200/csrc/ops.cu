@@ -244,6 +244,117 @@ void tgk_build(cudaStream_t s, int64_t n, const double* d, const double* e, doub
   BSE_LAUNCH_CHECK();
 }
 
+// Relative-accuracy refinement of the bidiagonal singular values (ascending, in place).
+// The TGK divide & conquer gives sigma to absolute accuracy eps*||B||; the reference's
+// zbdsqr gives high RELATIVE accuracy, which CHOL+SVD needs for its small eigenvalues
+// (test_solvers.cpp:188-199). Bisection on the Golub-Kahan matrix with
+// the LDL^T Sturm count is relatively accurate (Demmel-Kahan; LAPACK dbdsvdx). One warp per
+// singular value does 32-way multisection inside a bracket centred on the D&C value.
+__device__ __forceinline__ int tgk_count_below(int64_t n, const double* __restrict__ a2, double x,
+                                               double pivmin) {
+  // #eigenvalues of T_GK (zero diagonal, off-diagonal^2 a2[0..2n-2]) below x
+  int c = 0;
+  double q = -x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  c += q < 0.0;
+  for (int64_t k = 1; k < 2 * n; ++k) {
+    q = -x - a2[k - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    c += q < 0.0;
+  }
+  return c;
+}
+
+__global__ void tgk_a2_kernel(int64_t n, const double* __restrict__ d, const double* __restrict__ e,
+                              double scale, double* __restrict__ a2) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < 2 * n - 1;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const double v = ((k & 1) ? e[k >> 1] : d[k >> 1]) / scale;
+    a2[k] = v * v;
+  }
+}
+
+__global__ void tgk_refine_kernel(int64_t n, const double* __restrict__ a2, double scale,
+                                  double bound, double* __restrict__ sig) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const double pivmin = 1e-290;
+  const double s0 = sig[i] / scale;
+  const double tau = 64.0 * DBL_EPSILON * bound;
+  double lo = fmax(0.0, s0 - tau), hi = s0 + tau;
+  // verify the bracket: #(sigma < lo) <= i < #(sigma < hi)
+  {
+    int c = 0;
+    if (lane == 0) c = tgk_count_below(n, a2, lo, pivmin) - int(n);
+    else if (lane == 1) c = tgk_count_below(n, a2, hi, pivmin) - int(n);
+    const int clo = __shfl_sync(0xffffffffu, c, 0), chi = __shfl_sync(0xffffffffu, c, 1);
+    if (!(clo <= i && chi >= i + 1)) {
+      lo = 0.0;
+      hi = bound * (1.0 + 4.0 * DBL_EPSILON);
+    }
+  }
+  for (int it = 0; it < 40; ++it) {
+    if (hi - lo <= 2.0 * DBL_EPSILON * fmax(lo, hi) || hi - lo <= pivmin) break;
+    const double x = lo + (hi - lo) * double(lane + 1) / 33.0;
+    const int c = tgk_count_below(n, a2, x, pivmin) - int(n);
+    const unsigned ge = __ballot_sync(0xffffffffu, c >= i + 1);  // x above sigma_i
+    const int first = ge ? __ffs(ge) - 1 : 32;
+    const double nlo = first == 0 ? lo : lo + (hi - lo) * double(first) / 33.0;
+    const double nhi = first == 32 ? hi : lo + (hi - lo) * double(first + 1) / 33.0;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) sig[i] = 0.5 * (lo + hi) * scale;
+}
+
+__global__ void absmax_kernel(int64_t n, const double* __restrict__ d, const double* __restrict__ e,
+                              double* out) {
+  __shared__ double red[32];
+  double m = 0.0, g = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    m = fmax(m, fabs(d[k]));
+    if (k < n - 1) m = fmax(m, fabs(e[k]));
+    // Gershgorin bound of T_GK: |d_k| + |e_k|, |e_{k-1}| + |d_k|
+    const double l = k > 0 ? fabs(e[k - 1]) : 0.0, r = k < n - 1 ? fabs(e[k]) : 0.0;
+    g = fmax(g, fabs(d[k]) + fmax(l, r));
+  }
+  m = warp_max(m);
+  g = warp_max(g);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) mm = fmax(mm, red[w]);
+    out[0] = mm > 0.0 ? mm : 1.0;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = g;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double gg = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) gg = fmax(gg, red[w]);
+    out[1] = gg;
+  }
+}
+
+void tgk_refine(cudaStream_t s, int64_t n, const double* d, const double* e, double* sig,
+                double* scratch) {
+  if (n <= 0) return;
+  // scratch: [scale, gershgorin] + a2 (2n)
+  absmax_kernel<<<1, 1024, 0, s>>>(n, d, e, scratch);
+  BSE_LAUNCH_CHECK();
+  double h[2];
+  BSE_CUDA(cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, s));
+  BSE_CUDA(cudaStreamSynchronize(s));
+  double* a2 = scratch + 2;
+  tgk_a2_kernel<<<grid_for(2 * n), 256, 0, s>>>(n, d, e, h[0], a2);
+  BSE_LAUNCH_CHECK();
+  const int wpb = 8;
+  tgk_refine_kernel<<<unsigned(ceil_div(n, wpb)), 32 * wpb, 0, s>>>(n, a2, h[0], h[1] / h[0], sig);
+  BSE_LAUNCH_CHECK();
+}
+
 // Right-scale columns by r_j = 1/sqrt(lambda_j) (CHOL+SVD, solvers.cpp:152-156).
 __global__ void scale_cols_rsqrt_kernel(int64_t rows, int64_t cols, z_t* __restrict__ X,
                                         int64_t ldx, const double* __restrict__ lam) {

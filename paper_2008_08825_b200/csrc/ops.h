@@ -22,6 +22,10 @@ void tgk_build(cudaStream_t s, int64_t n, const double* d, const double* e, doub
                double* te);
 void tgk_extract(cudaStream_t s, int64_t n, const double* X, z_t* Ub, int64_t ldu, z_t* Vb,
                  int64_t ldv);
+// Relative-accuracy bisection refinement of ascending bidiagonal singular values (in place).
+// scratch: 2n + 2 doubles.
+void tgk_refine(cudaStream_t s, int64_t n, const double* d, const double* e, double* sig,
+                double* scratch);
 void scale_cols_rsqrt(cudaStream_t s, int64_t rows, int64_t cols, z_t* X, int64_t ldx,
                       const double* lam);
 void square_vec(cudaStream_t s, int64_t n, const double* a, double* b);

@@ -187,7 +187,7 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   double* d = w.take<double>(n);
   double* e = w.take<double>(n);
   double* td = w.take<double>(m2);
-  double* te = w.take<double>(m2);
+  double* te = w.take<double>(m2 + 8);
   z_t* tauq = w.take<z_t>(n);
   z_t* taup = w.take<z_t>(n);
   int* info = w.take<int>(4);
@@ -218,6 +218,7 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   clk.mark();
   // ascending singular values = top n TGK eigenvalues; vectors u (b3), v (b4)
   BSE_CUDA(cudaMemcpyAsync(sasc, td + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  tgk_refine(s, n, d, e, sasc, te);  // relative accuracy of the small singular values
   tgk_extract(s, n, X, b3, ld, b4, ld);
   zunmbr_q(s, n, b2, ld, tauq, b3, ld, n, ws_unmbr);  // U = Q U_B
   zunmbr_p(s, n, b2, ld, taup, b4, ld, n, ws_unmbr);  // V = P V_B

@@ -1,0 +1,77 @@
+// C++ drop-in check: the reference's test_solvers.cpp cases written against include/bse/*.hpp
+// (same names and exception classes), linked to libbse_b200.so. Exit code = failures.
+#include <cmath>
+#include <cstdio>
+
+#include "bse/backend.hpp"
+#include "bse/solvers.hpp"
+
+static int failures = 0;
+#define CHECK(c)                                                  \
+  do {                                                            \
+    if (!(c)) {                                                   \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c);     \
+      ++failures;                                                 \
+    }                                                             \
+  } while (0)
+
+static bse::Matrix scalar(double v) {
+  bse::Matrix m(1, 1);
+  m(0, 0) = v;
+  return m;
+}
+
+int main() {
+  using namespace bse;
+  const double s3 = std::sqrt(3.0);
+  for (Method m : {Method::Chol, Method::CholSvd}) {  // test_solvers.cpp:33-42
+    const SpectralResult r = solve(m, from_blocks(scalar(2.0), scalar(1.0)));
+    CHECK(std::abs(r.lambda[0] - s3) < 1e-13 * s3);
+    const Complex ph = r.v(0, 0) / std::abs(r.v(0, 0));
+    CHECK(std::abs(r.v(0, 0) / ph - 0.5 * (std::pow(3.0, 0.25) + std::pow(3.0, -0.25))) < 1e-12);
+    CHECK(std::abs(r.v(1, 0) / ph - 0.5 * (std::pow(3.0, -0.25) - std::pow(3.0, 0.25))) < 1e-12);
+  }
+  {  // decoupled B=0 (test_solvers.cpp:44-53)
+    Matrix a = Matrix::Zero(3, 3);
+    a(0, 0) = 3.0; a(1, 1) = 1.0; a(2, 2) = 2.0;
+    const SpectralResult r = solve_chol(from_blocks(a, Matrix::Zero(3, 3)));
+    CHECK(std::abs(r.lambda[0] - 1.0) < 1e-13 && std::abs(r.lambda[2] - 3.0) < 1e-13);
+  }
+  try {  // test_solvers.cpp:73-79
+    solve_chol_svd(from_blocks(scalar(1.0), scalar(2.0)));
+    CHECK(false);
+  } catch (const NotDefinite& e) {
+    CHECK(e.which() == Block::M2);
+    CHECK(std::string(error_kind(e)) == "NotDefinite");
+  }
+  try {  // test_backend.cpp:78-85
+    Matrix m(2, 2);
+    m(0, 0) = 1.0; m(0, 1) = 2.0; m(1, 0) = 2.0; m(1, 1) = 1.0;
+    cholesky_lower(m);
+    CHECK(false);
+  } catch (const NotPositiveDefinite& e) {
+    CHECK(e.pivot_index() == 1);
+  }
+  {  // clamp / flag (test_solvers.cpp:168-186)
+    Matrix a = Matrix::Zero(2, 2);
+    a(0, 0) = 1e-40; a(1, 1) = 1.0;
+    const SpectralResult r = solve_chol(from_blocks(a, Matrix::Zero(2, 2)));
+    CHECK(r.near_singular.size() == 1 && r.near_singular[0] == 0);
+    CHECK(std::abs(r.lambda[0] - machine_eps()) < 1e-6 * machine_eps());
+  }
+  {  // backend: [[2,1],[1,2]] -> (1, 3)
+    Matrix m(2, 2);
+    m(0, 0) = 2.0; m(0, 1) = 1.0; m(1, 0) = 1.0; m(1, 1) = 2.0;
+    const HermitianEig e = hermitian_eig(m);
+    CHECK(std::abs(e.values[0] - 1.0) < 1e-14 && std::abs(e.values[1] - 3.0) < 1e-14);
+    const Matrix p = matmul(m, m, {.op_a = Op::Adjoint});
+    CHECK(std::abs(p(0, 0) - Complex(5.0)) < 1e-14);
+  }
+  try {
+    solve_sqrt(from_blocks(scalar(2.0), scalar(1.0)));
+    CHECK(false);
+  } catch (const InvalidSpec&) {
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures;
+}

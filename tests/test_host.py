@@ -1,0 +1,182 @@
+"""CPU-side checks: the C-ABI library loads and exports every symbol include/bse_gpu.h
+declares, host-side validation mirrors the reference, generators are deterministic, and the
+compute entry points fail loudly (no CPU fallback) when no GPU is present."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2008_08825_b200 as bse
+from paper_2008_08825_b200 import _lib, configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "bse_gpu.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void\*|void)\s+(bse_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("bse_solve", "bse_solve_device", "bse_cholesky_lower", "bse_matmul",
+              "bse_tri_solve", "bse_hermitian_eig", "bse_svd", "bse_product_pair",
+              "bse_assemble_eigenvectors", "bse_ctx_create"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    for s in declared_symbols():
+        assert hasattr(L, s), s
+        assert s in _lib.SYMBOLS, f"{s} missing from the ctypes binding table"
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                        text=True).stdout
+    for s in declared_symbols():
+        assert re.search(rf"\bT {s}$", nm, re.M), s
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_abi_version():
+    assert _lib.lib().bse_abi_version() == 1
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device path")
+def test_no_cpu_fallback_without_gpu():
+    with pytest.raises(bse.DeviceError):
+        bse.Context(0)
+    h = bse.from_blocks(np.array([[2.0]]), np.array([[1.0]]))
+    with pytest.raises(bse.DeviceError):
+        bse.solve_chol(h)
+
+
+def test_from_blocks_validation():
+    """core.cpp:45-75 / SPEC.md from_blocks examples."""
+    h = bse.from_blocks(np.array([[2.0]]), np.array([[1.0]]))
+    assert h.n == 1 and h.a.flags.f_contiguous
+    with pytest.raises(bse.NotHermitian) as e:
+        bse.from_blocks(np.array([[0.0, 1.0], [0.0, 0.0]]), np.zeros((2, 2)))
+    assert e.value.relative_deviation > 1e-12
+    with pytest.raises(bse.DimensionMismatch):
+        bse.from_blocks(np.eye(2), np.eye(3))
+    with pytest.raises(bse.DimensionMismatch):
+        bse.from_blocks(np.zeros((2, 3)), np.zeros((2, 3)))
+    with pytest.raises(bse.DimensionMismatch):
+        bse.from_blocks(np.zeros((0, 0)), np.zeros((0, 0)))
+    # symmetrisation within tolerance
+    a = np.array([[1.0, 2.0 + 1e-14], [2.0, 3.0]])
+    h = bse.from_blocks(a, np.zeros((2, 2)))
+    assert h.a[0, 1] == h.a[1, 0]
+
+
+def test_method_names():
+    assert bse.method_name(bse.Method.CholSvd) == "chol-svd"
+    assert bse.method_from_name("cholsvd") == bse.Method.CholSvd
+    with pytest.raises(bse.InvalidSpec):
+        bse.method_from_name("qr")
+
+
+def test_negative_spectrum_host():
+    lam = np.array([1.0, 2.0])
+    v = np.arange(8, dtype=complex).reshape(4, 2)
+    h = bse.BseMatrixI(np.eye(2, dtype=complex), np.zeros((2, 2), complex))
+    neg = bse.negative_spectrum(h, bse.SpectralResult(lam, v, bse.Method.Chol, [1]))
+    assert np.array_equal(neg.lambda_, -lam)
+    assert np.array_equal(neg.v[:2], v[2:]) and np.array_equal(neg.v[2:], v[:2])
+    assert neg.near_singular == [1]
+    with pytest.raises(bse.DimensionMismatch):
+        bse.negative_spectrum(h, bse.SpectralResult(lam, v[:3], bse.Method.Chol))
+
+
+def _mt19937_64(seed):
+    """Pure-Python MT19937-64 (std::mt19937_64), to pin the C++ GaussianStream port."""
+    n, m = 312, 156
+    mt = [0] * n
+    mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+    for i in range(1, n):
+        mt[i] = (6364136223846793005 * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+    idx = n
+    while True:
+        if idx >= n:
+            for i in range(n):
+                x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % n] & 0x7FFFFFFF)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[i] = mt[(i + m) % n] ^ xa
+            idx = 0
+        y = mt[idx]
+        idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        yield y & 0xFFFFFFFFFFFFFFFF
+
+
+def _splitmix64_at(seed, k):
+    M = 0xFFFFFFFFFFFFFFFF
+    z = (seed + (k + 1) * 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def test_gaussian_stream_is_the_reference_stream():
+    """gen.cpp:8-38: splitmix64 -> mt19937_64 -> Box-Muller pairs, next_complex scaling."""
+    seed, stream = 11, 0
+    g = _mt19937_64(_splitmix64_at(seed, stream))
+    vals = []
+    for _ in range(3):
+        u1 = ((next(g) >> 11) + 1) * 2.0 ** -53
+        u2 = (next(g) >> 11) * 2.0 ** -53
+        r = np.sqrt(-2.0 * np.log(u1))
+        vals += [r * np.cos(2 * np.pi * u2), r * np.sin(2 * np.pi * u2)]
+    expect = (np.array(vals[0::2]) + 1j * np.array(vals[1::2])) * (np.sqrt(2) / 2)
+    got = configs.gaussian_stream(seed, stream, 3)
+    assert np.allclose(got, expect, rtol=1e-15, atol=1e-15)
+
+
+def test_config_generators_deterministic_and_hermitian():
+    a1, b1 = configs.config2(5, n=33)
+    a2, b2 = configs.config2(5, n=33)
+    assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
+    assert np.allclose(a1, a1.conj().T, atol=0) and np.allclose(b1, b1.conj().T, atol=0)
+    d = np.diag(a1).real  # d ~ U[1,20] plus O(0.1/sqrt n) noise
+    assert d.min() > 0.5 and d.max() < 21
+    a, b = configs.config1(0, n=16)
+    assert np.all(a.imag == 0) and np.all(b.imag == 0)
+    a3, b3 = configs.config3(0, n=24)
+    m2 = a3 - b3
+    w = np.linalg.eigvalsh(m2)
+    assert np.allclose(np.sort(w), np.logspace(-6, 1, 24), rtol=1e-6, atol=1e-12)
+    a4, _ = configs.config2(6, n=16)
+    assert not np.array_equal(a4, a1[:16, :16])
+
+
+def test_cpp_dropin_headers_compile(tmp_path):
+    """include/bse/*.hpp (the C++ drop-in API) compile standalone against the C-ABI."""
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "bse/solvers.hpp"\n#include "bse/backend.hpp"\n'
+                   'int main() { bse::Matrix a(1, 1); a(0, 0) = 2.0; '
+                   'auto h = bse::from_blocks(a, bse::Matrix(1, 1)); (void)h; return 0; }\n')
+    r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", f"-I{ROOT}/include", str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
