@@ -28,9 +28,11 @@ namespace cg = cooperative_groups;
 namespace bseg {
 
 namespace {
-constexpr int kT = 64;     // hemv tile
-constexpr int kRB = 256;   // row block of phases 1/3 (= threads per CTA)
-constexpr int kThreads = 256;
+constexpr int kT = 64;         // hemv tile edge = row slab of the vector phases
+constexpr int kThreads = 256;  // 4 threads per slab row
+constexpr int NB = kHetrdNB;   // panel width (compile-time: fully unrolled panel loops)
+constexpr int kQ = kThreads / kT;
+static_assert(NB % kQ == 0 && NB <= 32, "panel width");
 }  // namespace
 
 struct HetrdArgs {
@@ -42,15 +44,13 @@ struct HetrdArgs {
   z_t* VW;  // n x 2NB: [V | W]
   z_t* WV;  // n x 2NB: [W | V]
   int64_t ldp;
-  z_t* wtmp;      // n   : unscaled-then-tau'd w before the alpha correction
-  z_t* Y;         // nch * nch * kT
-  double* normp;  // nrb
-  z_t* s1p;       // nrb x NB
-  z_t* s2p;       // nrb x NB
-  z_t* t12;       // 2 NB
-  z_t* dotp;      // nrb
+  z_t* Y;         // nch * nch * kT: hemv tile partials [row chunk][col chunk]
+  double* normp;  // nch : partial ||x||^2 of the next reflector's tail, per slab
+  z_t* s12p;      // nch x 2NB: per-slab partial W^H x | V^H x
+  z_t* t12;       // 2NB : t1 = W^H v | t2 = V^H v
+  double* vav;    // gridDim.x : per-CTA partials of v^H A22 v
   int64_t p0;
-  int nbp, nb, nch, nrb;
+  int nbp, nch;
 };
 
 __device__ __forceinline__ z_t zdiv1(z_t a) {  // 1 / a
@@ -73,115 +73,77 @@ __device__ __forceinline__ void larfg_params(z_t alpha, double xnorm2, double& b
   scale = zdiv1(make_double2(alpha.x - beta, alpha.y));
 }
 
-__global__ void __launch_bounds__(kThreads) hetrd_panel_kernel(HetrdArgs a) {
+// Warp-parallel fixed-order sums (every warp of every CTA gets bit-identical results).
+__device__ __forceinline__ double warp_sum_range(const double* p, int lo, int hi) {
+  double s = 0.0;
+  for (int k = lo + (threadIdx.x & 31); k < hi; k += 32) s += p[k];
+  return warp_sum(s);
+}
+
+__device__ __forceinline__ int first_owned(int lo, int cta, int G) {
+  return lo + ((cta - lo % G) % G + G) % G;
+}
+
+// One cooperative launch per nb-column panel. Per column g (index i in the panel):
+//   phase A : reflector from the partial norms (zlarfg, redundantly per CTA), v into the
+//             panel, Hermitian mat-vec y = A22 v over 64x64 lower tiles (each tile adds
+//             A_t v to its row chunk and A_t^H v to its column chunk) + per-CTA v^H A22 v;
+//   phase B : alpha = -1/2 |tau|^2 (v^H A v - 2 Re t1^H t2) (no separate dot reduction),
+//             W(:,i) = tau (y - V t1 - W t2) + alpha v, and the NEXT column's update
+//             a(:,g+1) -= V W(g+1,:)^H + W V(g+1,:)^H with its partial norms / W^H x / V^H x.
+// => two grid barriers per column; every partial sum has a fixed order (deterministic).
+__global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char sm[];
   z_t* tile = reinterpret_cast<z_t*>(sm);  // kT x (kT+1) column-major
-  z_t* vr = tile + kT * (kT + 1);          // kT : v over tile rows
-  z_t* vc = vr + kT;                       // kT : v over tile cols
-  z_t* red = vc + kT;                      // 4 x kT reduction scratch
-  z_t* wg = red + 4 * kT;                  // NB : W(g, p)
-  z_t* vg = wg + 64;                       // NB : V(g, p)
-  z_t* xs = vg + 64;                       // kRB : updated column values
-  double* dred = reinterpret_cast<double*>(xs + kRB);  // 32 doubles
-  z_t* zred = reinterpret_cast<z_t*>(dred + 32);        // 8 x 64 complex
+  z_t* vr = tile + kT * (kT + 1);          // v over tile rows
+  z_t* vc = vr + kT;                       // v over tile cols
+  z_t* red = vc + kT;                      // kQ x kT reduction scratch
+  z_t* red2 = red + kQ * kT;               // kQ x kT reduction scratch
+  z_t* wg = red2 + kQ * kT;                // NB : W(g+1, p)
+  z_t* vg = wg + NB;                       // NB : V(g+1, p)
+  z_t* xs = vg + NB;                       // kT : next column values of the slab
+  z_t* wc = xs + kT;                       // kT : W(r, i) of the slab
+  z_t* tt = wc + kT;                       // 2NB : t1 | t2
+  z_t* zred = tt + 2 * NB;                 // 8 complex
+  double* dred = reinterpret_cast<double*>(zred + 8);  // 8 doubles
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rl = tid & (kT - 1), q = tid / kT;
   const int G = gridDim.x, cta = blockIdx.x;
   const int64_t n = a.n, lda = a.lda, ldp = a.ldp;
-  const int NB = a.nb;
   z_t* V = a.VW;
   z_t* W = a.VW + int64_t(NB) * ldp;
+  const z_t zero = make_double2(0.0, 0.0);
 
-  for (int i = 0; i <= a.nbp; ++i) {
-    const int64_t g = a.p0 + i;
-    const bool last = (i == a.nbp);  // finalisation-only step
-    // ------------------------------------------------------------------ phase 1
-    z_t alpha_prev = make_double2(0.0, 0.0);
-    if (i > 0) {
-      z_t dot = make_double2(0.0, 0.0);
-      for (int rb = int(g / kRB); rb < a.nrb; ++rb) dot = zadd(dot, a.dotp[rb]);
-      const z_t tp = a.tau[g - 1];
-      alpha_prev = zscale(zmul(tp, dot), -0.5);
-    }
-    // row g of V and W (W(g, i-1) finalised here redundantly)
-    if (!last) {
-      for (int p = tid; p < i; p += blockDim.x) {
-        z_t vgp = V[g + int64_t(p) * ldp];
-        z_t wgp;
-        if (p == i - 1) wgp = zadd(a.wtmp[g], zmul(alpha_prev, vgp));
-        else wgp = W[g + int64_t(p) * ldp];
-        wg[p] = wgp;
-        vg[p] = vgp;
-      }
-    }
-    __syncthreads();
-    for (int rb = cta; rb < a.nrb; rb += G) {
-      const int64_t r = int64_t(rb) * kRB + tid;
-      const int64_t rlo = last ? g : g;  // rows >= g
-      const bool valid = r < n && r >= rlo;
-      z_t wprev = make_double2(0.0, 0.0);
-      if (i > 0 && valid) {
-        wprev = zadd(a.wtmp[r], zmul(alpha_prev, V[r + int64_t(i - 1) * ldp]));
-        W[r + int64_t(i - 1) * ldp] = wprev;
-        a.WV[r + int64_t(i - 1) * ldp] = wprev;
-      }
-      if (last) continue;
-      z_t x = make_double2(0.0, 0.0);
-      if (valid) {
+  // ---------------------------------------------------------------- phase 0: column p0
+  {
+    const int64_t g = a.p0;
+    for (int c = first_owned(int(g / kT), cta, G); c < a.nch; c += G) {
+      const int64_t r = int64_t(c) * kT + rl;
+      z_t x = zero;
+      if (q == 0 && r < n && r >= g) {
         x = a.A[r + g * lda];
-        for (int p = 0; p < i; ++p) {
-          const z_t vrp = V[r + int64_t(p) * ldp];
-          const z_t wrp = (p == i - 1) ? wprev : W[r + int64_t(p) * ldp];
-          // x -= V(r,p) conj(W(g,p)) + W(r,p) conj(V(g,p))
-          const z_t t1 = zmul(vrp, zconj(wg[p]));
-          const z_t t2 = zmul(wrp, zconj(vg[p]));
-          x = zsub(x, zadd(t1, t2));
-        }
         if (r == g) {
           x.y = 0.0;
+          a.A[r + g * lda] = x;
           a.d[g] = x.x;
         }
-        a.A[r + g * lda] = x;
       }
-      const bool inx = valid && r >= g + 2;
-      xs[tid] = inx ? x : make_double2(0.0, 0.0);
+      const bool inx = q == 0 && r < n && r >= g + 2;
       const double nrm = block_sum(inx ? zabs2(x) : 0.0, dred);
-      if (tid == 0) a.normp[rb] = nrm;
-      // s1[p] = sum conj(W(r,p)) x(r), s2[p] = sum conj(V(r,p)) x(r), r in this block
-      for (int p = warp; p < i; p += kThreads / 32) {
-        z_t s1 = make_double2(0.0, 0.0), s2 = make_double2(0.0, 0.0);
-        for (int j = lane; j < kRB; j += 32) {
-          const int64_t rr = int64_t(rb) * kRB + j;
-          if (rr >= g + 2 && rr < n) {
-            const z_t xv = xs[j];
-            const z_t wv = (p == i - 1) ? zadd(a.wtmp[rr], zmul(alpha_prev, V[rr + int64_t(p) * ldp]))
-                                        : W[rr + int64_t(p) * ldp];
-            zcfma(s1, wv, xv);
-            zcfma(s2, V[rr + int64_t(p) * ldp], xv);
-          }
-        }
-        s1 = warp_zsum(s1);
-        s2 = warp_zsum(s2);
-        if (lane == 0) {
-          a.s1p[int64_t(rb) * NB + p] = s1;
-          a.s2p[int64_t(rb) * NB + p] = s2;
-        }
-      }
-      __syncthreads();
+      if (tid == 0) a.normp[c] = nrm;
     }
-    if (last) break;
-    grid.sync();
-    // ------------------------------------------------------------------ phase 2
-    if (g + 1 >= n) {
-      // last column: no reflector; e/tau undefined
-      grid.sync();
-      grid.sync();
-      continue;
-    }
-    double xn2 = 0.0;
-    for (int rb = int(g / kRB); rb < a.nrb; ++rb) xn2 += a.normp[rb];
-    const z_t alpha = a.A[(g + 1) + g * lda];
+  }
+  grid.sync();
+
+  for (int i = 0; i < a.nbp; ++i) {
+    const int64_t g = a.p0 + i;
+    const int64_t g1 = g + 1;
+    const bool has_next = (i + 1 < a.nbp);
+    // ---------------------------------------------------------------- phase A
+    const double xn2 = warp_sum_range(a.normp, int(g / kT), a.nch);
+    const z_t alpha = a.A[g1 + g * lda];  // g + 1 < n always (panels stop at n-2)
     double beta;
     z_t tau, scale;
     larfg_params(alpha, xn2, beta, tau, scale);
@@ -191,34 +153,42 @@ __global__ void __launch_bounds__(kThreads) hetrd_panel_kernel(HetrdArgs a) {
         a.tau[g] = tau;
       }
       // t1 = W^H v, t2 = V^H v over rows >= g+1 (v(g+1) = 1, v(r) = scale x(r))
-      for (int p = tid; p < i; p += blockDim.x) {
-        z_t s1 = make_double2(0.0, 0.0), s2 = make_double2(0.0, 0.0);
-        for (int rb = int(g / kRB); rb < a.nrb; ++rb) {
-          s1 = zadd(s1, a.s1p[int64_t(rb) * NB + p]);
-          s2 = zadd(s2, a.s2p[int64_t(rb) * NB + p]);
+      const int kk = tid >> 2, part = tid & 3;  // 64 sums x 4 partial lanes
+      const int p = kk & (NB - 1);
+      z_t s = zero;
+      if (p < i)
+        for (int c = int(g / kT) + part; c < a.nch; c += 4)
+          s = zadd(s, a.s12p[int64_t(c) * 2 * NB + kk]);
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
+      if (part == 0 && kk < 2 * NB) {
+        z_t t = zero;
+        if (p < i) {
+          const z_t head = kk < NB ? W[g1 + int64_t(p) * ldp] : V[g1 + int64_t(p) * ldp];
+          t = zadd(zconj(head), zmul(scale, s));
         }
-        const z_t w1 = W[(g + 1) + int64_t(p) * ldp];
-        const z_t v1 = V[(g + 1) + int64_t(p) * ldp];
-        a.t12[p] = zadd(zconj(w1), zmul(scale, s1));
-        a.t12[NB + p] = zadd(zconj(v1), zmul(scale, s2));
+        a.t12[kk] = t;
       }
     }
-    // reflector vector into the panels (own row blocks)
-    for (int rb = cta; rb < a.nrb; rb += G) {
-      const int64_t r = int64_t(rb) * kRB + tid;
-      if (r < n) {
-        z_t v = make_double2(0.0, 0.0);
-        if (r == g + 1) v = make_double2(1.0, 0.0);
-        else if (r >= g + 2) v = zmul(scale, a.A[r + g * lda]);
-        V[r + int64_t(i) * ldp] = v;
-        a.WV[r + int64_t(NB + i) * ldp] = v;
+    // reflector vector into the panels (rows >= g+1 of the owned slabs)
+    if (q == 0) {
+      for (int c = first_owned(int(g1 / kT), cta, G); c < a.nch; c += G) {
+        const int64_t r = int64_t(c) * kT + rl;
+        if (r < n && r >= g1) {
+          const z_t v = (r == g1) ? make_double2(1.0, 0.0) : zmul(scale, a.A[r + g * lda]);
+          V[r + int64_t(i) * ldp] = v;
+          a.WV[r + int64_t(NB + i) * ldp] = v;
+        }
       }
     }
     // hemv over lower tiles of the trailing matrix rows/cols [g+1, n)
     {
-      const int c0 = int((g + 1) / kT);
+      const int c0 = int(g1 / kT);
       const int K = a.nch - c0;
       const int64_t ntiles = int64_t(K) * (K + 1) / 2;
+      double vav = 0.0;
       for (int64_t t = cta; t < ntiles; t += G) {
         int bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
         while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
@@ -227,103 +197,187 @@ __global__ void __launch_bounds__(kThreads) hetrd_panel_kernel(HetrdArgs a) {
         const int64_t R0 = int64_t(c0 + bi) * kT, C0 = int64_t(c0 + bj) * kT;
         const bool diag = (bi == bj);
         __syncthreads();
-        // v over rows and cols of the tile
-        if (tid < kT) {
-          const int64_t r = R0 + tid;
-          z_t v = make_double2(0.0, 0.0);
-          if (r == g + 1) v = make_double2(1.0, 0.0);
-          else if (r >= g + 2 && r < n) v = zmul(scale, a.A[r + g * lda]);
-          vr[tid] = v;
-        } else if (tid < 2 * kT) {
-          const int64_t c = C0 + (tid - kT);
-          z_t v = make_double2(0.0, 0.0);
-          if (c == g + 1) v = make_double2(1.0, 0.0);
-          else if (c >= g + 2 && c < n) v = zmul(scale, a.A[c + g * lda]);
-          vc[tid - kT] = v;
-        }
-        // tile load (masked: rows/cols >= g+1, < n, lower incl. diagonal)
-        for (int e = tid; e < kT * kT; e += kThreads) {
-          const int rr = e % kT, cc = e / kT;
-          const int64_t r = R0 + rr, c = C0 + cc;
-          z_t val = make_double2(0.0, 0.0);
-          if (r < n && c < n && c >= g + 1 && r >= g + 1 && r >= c) {
-            val = a.A[r + c * lda];
-            if (r == c) val.y = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < kT * kT / kThreads; ++k) {
+          const int e2 = tid + k * kThreads;
+          const int rr = e2 % kT, cc = e2 / kT;
+          const int64_t r = R0 + rr, cl = C0 + cc;
+          z_t val = zero;
+          if (r < n && cl < n && cl >= g1 && r >= cl) {
+            val = a.A[r + cl * lda];
+            if (r == cl) val.y = 0.0;
           }
           tile[rr + cc * (kT + 1)] = val;
         }
-        __syncthreads();
-        // y_R(r) = sum_c A(r,c) v(c) ; y_C(c) = sum_{r} conj(A(r,c)) v(r) (strictly lower if diag)
-        const int q = tid >> 6, x = tid & 63;
-        z_t yr = make_double2(0.0, 0.0), yc = make_double2(0.0, 0.0);
-        for (int k = q * 16; k < q * 16 + 16; ++k) {
-          zfma(yr, tile[x + k * (kT + 1)], vc[k]);
-          if (!diag || k > x) zcfma(yc, tile[k + x * (kT + 1)], vr[k]);
-        }
-        red[q * kT + x] = yr;
-        __syncthreads();
-        if (q == 0) {
-          z_t s = red[x];
-          s = zadd(s, red[kT + x]);
-          s = zadd(s, red[2 * kT + x]);
-          s = zadd(s, red[3 * kT + x]);
-          yr = s;
+        if (tid < kT) {
+          const int64_t r = R0 + tid;
+          z_t v = zero;
+          if (r == g1) v = make_double2(1.0, 0.0);
+          else if (r > g1 && r < n) v = zmul(scale, a.A[r + g * lda]);
+          vr[tid] = v;
+        } else if (tid < 2 * kT) {
+          const int64_t cl = C0 + (tid - kT);
+          z_t v = zero;
+          if (cl == g1) v = make_double2(1.0, 0.0);
+          else if (cl > g1 && cl < n) v = zmul(scale, a.A[cl + g * lda]);
+          vc[tid - kT] = v;
         }
         __syncthreads();
-        red[q * kT + x] = yc;
+        z_t yr = zero, yc = zero;
+#pragma unroll 4
+        for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) {
+          zfma(yr, tile[rl + k * (kT + 1)], vc[k]);
+          if (!diag || k > rl) zcfma(yc, tile[k + rl * (kT + 1)], vr[k]);
+        }
+        red[q * kT + rl] = yr;
+        red2[q * kT + rl] = yc;
         __syncthreads();
         if (q == 0) {
-          z_t s = red[x];
-          s = zadd(s, red[kT + x]);
-          s = zadd(s, red[2 * kT + x]);
-          s = zadd(s, red[3 * kT + x]);
-          yc = s;
+          z_t sr = red[rl], sc = red2[rl];
+#pragma unroll
+          for (int qq = 1; qq < kQ; ++qq) {
+            sr = zadd(sr, red[qq * kT + rl]);
+            sc = zadd(sc, red2[qq * kT + rl]);
+          }
           const int gi = c0 + bi, gj = c0 + bj;
           if (diag) {
-            a.Y[(int64_t(gi) * a.nch + gi) * kT + x] = zadd(yr, yc);
+            a.Y[(int64_t(gi) * a.nch + gi) * kT + rl] = zadd(sr, sc);
           } else {
-            a.Y[(int64_t(gi) * a.nch + gj) * kT + x] = yr;
-            a.Y[(int64_t(gj) * a.nch + gi) * kT + x] = yc;
+            a.Y[(int64_t(gi) * a.nch + gj) * kT + rl] = sr;
+            a.Y[(int64_t(gj) * a.nch + gi) * kT + rl] = sc;
+          }
+          // v^H (A v) contributions of this tile: rows R (A_t v_C) and, mirrored, cols C
+          const z_t cr = zcmul(vr[rl], sr), cc2 = zcmul(vc[rl], sc);
+          vav += cr.x + cc2.x;
+        }
+      }
+      const double vtot = block_sum(vav, dred);
+      if (tid == 0) a.vav[cta] = vtot;
+    }
+    grid.sync();
+    // ---------------------------------------------------------------- phase B
+    const double vav = warp_sum_range(a.vav, 0, G);
+    if (tid < 2 * NB) tt[tid] = a.t12[tid];  // zero beyond i
+    __syncthreads();
+    // v^H w' = v^H A v - sum_p [conj(t2_p) t1_p + conj(t1_p) t2_p]  (real)
+    double vw = vav;
+#pragma unroll
+    for (int p = 0; p < NB; ++p) {
+      if (p < i) {
+        const z_t c = zcmul(tt[NB + p], tt[p]);
+        vw -= 2.0 * c.x;
+      }
+    }
+    const double tau2 = zabs2(tau);
+    const double alw = -0.5 * tau2 * vw;  // alpha of W = tau w' + alpha v (real)
+    const int c0 = int(g1 / kT);
+    // row g+1 of V and W (W(g+1, i) redundantly in every CTA, fixed order)
+    if (warp == 0) {
+      z_t y = zero;
+      const int cg1 = int(g1 / kT), off = int(g1 % kT);
+      for (int b = c0 + lane; b < a.nch; b += 32) y = zadd(y, a.Y[(int64_t(cg1) * a.nch + b) * kT + off]);
+      z_t corr = zero;
+      z_t vgp = zero, wgp = zero;
+      if (lane < i) {
+        vgp = V[g1 + int64_t(lane) * ldp];
+        wgp = W[g1 + int64_t(lane) * ldp];
+        corr = zadd(zmul(vgp, tt[lane]), zmul(wgp, tt[NB + lane]));
+      }
+      y = warp_zsum(y);
+      corr = warp_zsum(corr);
+      if (lane < NB) {
+        vg[lane] = lane < i ? vgp : (lane == i ? make_double2(1.0, 0.0) : zero);
+        wg[lane] = lane < i ? wgp : zero;
+      }
+      if (lane == 0) wg[i] = make_double2(zmul(tau, zsub(y, corr)).x + alw,
+                                         zmul(tau, zsub(y, corr)).y);
+    }
+    __syncthreads();
+    for (int c = first_owned(c0, cta, G); c < a.nch; c += G) {
+      const int64_t r = int64_t(c) * kT + rl;
+      const bool valid = r < n && r >= g1;
+      z_t ypart = zero, upd = zero, vri = zero, xold = zero;
+      if (valid) {
+        if (q == 0) {
+          vri = V[r + int64_t(i) * ldp];
+          if (has_next) xold = a.A[r + g1 * lda];
+        }
+        for (int b = c0 + q; b < a.nch; b += kQ) ypart = zadd(ypart, a.Y[(int64_t(c) * a.nch + b) * kT + rl]);
+#pragma unroll
+        for (int k = 0; k < NB / kQ; ++k) {
+          const int p = q + k * kQ;
+          if (p < i) {
+            const z_t vrp = V[r + int64_t(p) * ldp], wrp = W[r + int64_t(p) * ldp];
+            ypart = zsub(ypart, zadd(zmul(vrp, tt[p]), zmul(wrp, tt[NB + p])));
+            upd = zadd(upd, zadd(zmul(vrp, zconj(wg[p])), zmul(wrp, zconj(vg[p]))));
           }
         }
       }
-    }
-    grid.sync();
-    // ------------------------------------------------------------------ phase 3
-    {
-      const int c0 = int((g + 1) / kT);
-      for (int rb = cta; rb < a.nrb; rb += G) {
-        const int64_t r = int64_t(rb) * kRB + tid;
-        const bool valid = r < n && r >= g + 1;
-        z_t w = make_double2(0.0, 0.0), v = make_double2(0.0, 0.0);
+      red[q * kT + rl] = ypart;
+      red2[q * kT + rl] = upd;
+      __syncthreads();
+      z_t xn = zero;
+      if (q == 0) {
+        z_t wri = zero;
         if (valid) {
-          const int ch = int(r / kT), off = int(r % kT);
-          z_t y = make_double2(0.0, 0.0);
-          for (int b = c0; b < a.nch; ++b) y = zadd(y, a.Y[(int64_t(ch) * a.nch + b) * kT + off]);
-          for (int p = 0; p < i; ++p) {
-            y = zsub(y, zmul(V[r + int64_t(p) * ldp], a.t12[p]));
-            y = zsub(y, zmul(W[r + int64_t(p) * ldp], a.t12[NB + p]));
+          z_t y = red[rl], u = red2[rl];
+#pragma unroll
+          for (int qq = 1; qq < kQ; ++qq) {
+            y = zadd(y, red[qq * kT + rl]);
+            u = zadd(u, red2[qq * kT + rl]);
           }
-          w = zmul(tau, y);
-          a.wtmp[r] = w;
-          v = V[r + int64_t(i) * ldp];
-          if (r >= g + 2) a.A[r + g * lda] = v;  // reflector storage below the subdiagonal
+          wri = zadd(zmul(tau, y), zscale(vri, alw));
+          if (r == g1) wri = wg[i];  // the value every CTA used for row g+1
+          W[r + int64_t(i) * ldp] = wri;
+          a.WV[r + int64_t(i) * ldp] = wri;
+          if (r >= g1 + 1) a.A[r + g * lda] = vri;  // reflector storage below the subdiagonal
+          if (has_next) {
+            // a(r, g+1) -= sum_{p<=i} V(r,p) conj(W(g+1,p)) + W(r,p) conj(V(g+1,p))
+            z_t x = zsub(xold, u);
+            x = zsub(x, zadd(zmul(vri, zconj(wg[i])), wri));  // p = i, V(g+1,i) = 1
+            if (r == g1) {
+              x.y = 0.0;
+              a.d[g1] = x.x;
+            }
+            a.A[r + g1 * lda] = x;
+            if (r >= g1 + 2) xn = x;
+          }
         }
-        // dot partial: conj(w) v
-        z_t pd = make_double2(0.0, 0.0);
-        if (valid) zcfma(pd, w, v);
-        pd = warp_zsum(pd);
-        __syncthreads();
-        if (lane == 0) zred[warp] = pd;
-        __syncthreads();
-        if (tid == 0) {
-          z_t s = make_double2(0.0, 0.0);
-          for (int ww = 0; ww < kThreads / 32; ++ww) s = zadd(s, zred[ww]);
-          a.dotp[rb] = s;
+        xs[rl] = xn;
+        wc[rl] = wri;
+      }
+      if (has_next) {
+        const double nrm = block_sum(q == 0 ? zabs2(xn) : 0.0, dred);  // syncs: xs, wc visible
+        if (tid == 0) a.normp[c] = nrm;
+        // s1[p] = sum conj(W(r,p)) x(r), s2[p] = sum conj(V(r,p)) x(r), p <= i, over the slab
+#pragma unroll
+        for (int k = 0; k < NB / 8; ++k) {
+          const int p = warp + 8 * k;
+          if (p <= i) {
+            z_t s1 = zero, s2 = zero;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = lane + 32 * h;
+              const int64_t rr = int64_t(c) * kT + j;
+              if (rr < n) {
+                const z_t xv = xs[j];
+                const z_t wv = (p == i) ? wc[j] : W[rr + int64_t(p) * ldp];
+                zcfma(s1, wv, xv);
+                zcfma(s2, V[rr + int64_t(p) * ldp], xv);
+              }
+            }
+            s1 = warp_zsum(s1);
+            s2 = warp_zsum(s2);
+            if (lane == 0) {
+              a.s12p[int64_t(c) * 2 * NB + p] = s1;
+              a.s12p[int64_t(c) * 2 * NB + NB + p] = s2;
+            }
+          }
         }
       }
+      __syncthreads();
     }
-    grid.sync();
+    if (has_next) grid.sync();
   }
 }
 
@@ -332,40 +386,34 @@ __global__ void set_last_diag_kernel(const z_t* A, int64_t lda, int64_t n, doubl
 }
 
 size_t hetrd_workspace_bytes(int64_t n) {
-  const int64_t nb = kHetrdNB;
-  const int64_t nch = ceil_div(n, kT), nrb = ceil_div(n, kRB);
+  const int64_t nch = ceil_div(n, kT);
   size_t z = 0;
-  z += size_t(n) * 2 * nb * 2;           // VW, WV
-  z += size_t(n);                        // wtmp
-  z += size_t(nch) * nch * kT;           // Y
-  z += size_t(nrb) * nb * 2;             // s1p, s2p
-  z += size_t(2 * nb);                   // t12
-  z += size_t(nrb);                      // dotp
-  return z * sizeof(z_t) + size_t(nrb) * sizeof(double) + 256;
+  z += size_t(n) * 2 * NB * 2;  // VW, WV
+  z += size_t(nch) * nch * kT;  // Y
+  z += size_t(nch) * 2 * NB;    // s12p
+  z += size_t(2 * NB);          // t12
+  return z * sizeof(z_t) + size_t(nch) * sizeof(double) + 4096 * sizeof(double) + 512;
 }
 
 void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, double* e,
                   z_t* tau, void* ws) {
   if (n <= 0) return;
-  const int nb = kHetrdNB;
-  const int nch = int(ceil_div(n, kT)), nrb = int(ceil_div(n, kRB));
+  const int nch = int(ceil_div(n, kT));
   z_t* base = reinterpret_cast<z_t*>(ws);
   HetrdArgs a{};
   a.A = A; a.lda = lda; a.n = n; a.d = d; a.e = e; a.tau = tau;
   a.ldp = n;
-  a.VW = base; base += n * 2 * nb;
-  a.WV = base; base += n * 2 * nb;
-  a.wtmp = base; base += n;
+  a.VW = base; base += n * 2 * NB;
+  a.WV = base; base += n * 2 * NB;
   a.Y = base; base += int64_t(nch) * nch * kT;
-  a.s1p = base; base += int64_t(nrb) * nb;
-  a.s2p = base; base += int64_t(nrb) * nb;
-  a.t12 = base; base += 2 * nb;
-  a.dotp = base; base += nrb;
+  a.s12p = base; base += int64_t(nch) * 2 * NB;
+  a.t12 = base; base += 2 * NB;
   a.normp = reinterpret_cast<double*>(base);
-  a.nb = nb; a.nch = nch; a.nrb = nrb;
+  a.vav = a.normp + nch;
+  a.nch = nch;
 
-  const size_t smem = (size_t(kT) * (kT + 1) + 2 * kT + 4 * kT + 128 + kRB) * sizeof(z_t) +
-                      32 * sizeof(double) + 8 * 64 * sizeof(z_t);
+  const size_t smem = (size_t(kT) * (kT + 1) + 2 * kT + 2 * kQ * kT + 2 * NB + 2 * kT + 2 * NB + 8) *
+                          sizeof(z_t) + 8 * sizeof(double);
   static int blocks_per_sm = -1;
   static int num_sms = 0;
   if (blocks_per_sm < 0) {
@@ -378,16 +426,21 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
                                                            kThreads, smem));
     if (blocks_per_sm < 1) throw std::runtime_error("hetrd: kernel cannot be resident");
   }
+  if (n == 1) {
+    set_last_diag_kernel<<<1, 32, 0, s>>>(A, lda, n, d);
+    BSE_LAUNCH_CHECK();
+    return;
+  }
   const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
-  for (int64_t p0 = 0; p0 < n - 1; p0 += nb) {
-    const int nbp = int(min64(nb, n - 1 - p0));
-    BSE_CUDA(cudaMemsetAsync(a.VW, 0, sizeof(z_t) * size_t(n) * 2 * nb * 2, s));
+  for (int64_t p0 = 0; p0 < n - 1; p0 += NB) {
+    const int nbp = int(min64(NB, n - 1 - p0));
+    BSE_CUDA(cudaMemsetAsync(a.VW, 0, sizeof(z_t) * size_t(n) * 2 * NB * 2, s));
     a.p0 = p0;
     a.nbp = nbp;
     // shrink the grid with the trailing size (fewer CTAs => cheaper grid barriers)
     const int64_t m = n - p0;
     const int64_t tiles = ceil_div(m, kT) * (ceil_div(m, kT) + 1) / 2;
-    int G = int(min64(int64_t(blocks_per_sm) * num_sms, max64(tiles, ceil_div(m, kRB))));
+    int G = int(min64(min64(int64_t(blocks_per_sm) * num_sms, 4096), tiles));
     G = max(G, 1);
     void* args[] = {&a};
     double bytes = 0.0;  // algorithmic: lower triangle of each column's trailing matrix
@@ -402,7 +455,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     count_launch();
     const int64_t q = p0 + nbp;
     if (q < n) {
-      zgemm(s, 0, 1, n - q, n - q, 2 * nb, mone, a.VW + q, n, a.WV + q, n, one, A + q + q * lda,
+      zgemm(s, 0, 1, n - q, n - q, 2 * NB, mone, a.VW + q, n, a.WV + q, n, one, A + q + q * lda,
             lda, kGeneral, kGeneral, 1, nullptr, 0);
     }
   }

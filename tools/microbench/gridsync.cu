@@ -1,0 +1,22 @@
+// grid.sync() latency probe (cooperative launch), B200.
+#include <cooperative_groups.h>
+#include <cstdio>
+namespace cg = cooperative_groups;
+__global__ void k(int iters, int* out) {
+  cg::grid_group g = cg::this_grid();
+  for (int i = 0; i < iters; ++i) g.sync();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = iters;
+}
+int main() {
+  int* out; cudaMalloc(&out, 4);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int G : {148, 296}) for (int T : {256}) {
+    int iters = 2000; void* args[] = {&iters, &out};
+    cudaLaunchCooperativeKernel((void*)k, G, T, args, 0, 0);
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel((void*)k, G, T, args, 0, 0);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("G=%d T=%d grid.sync = %.3f us (%s)\n", G, T, ms * 1000 / iters, cudaGetErrorString(cudaGetLastError()));
+  }
+}
