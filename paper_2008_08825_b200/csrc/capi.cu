@@ -176,6 +176,9 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
   try {
     BSE_CUDA(cudaSetDevice(device));
     BSE_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    BSE_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    BSE_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    BSE_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& ev : c->ev) BSE_CUDA(cudaEventCreate(&ev));
   } catch (const CudaError& ex) {
     delete c;
@@ -193,6 +196,12 @@ int bse_ctx_destroy(bse_ctx* c) {
   for (auto& ev : c->timer_events) cudaEventDestroy(ev);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+  }
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return BSE_OK;

@@ -15,6 +15,9 @@ struct bse_ctx {
   int64_t launches = 0;
   bse_phase_times last{};
   cudaEvent_t ev[12]{};
+  // second stream for independent stages (fork/join through fork_ev / join_ev)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::mutex mu;
   // live per-kernel timing (bse_ctx_set_kernel_timing)
   bool timing = false;
@@ -41,6 +44,17 @@ struct Bump {
 
 // Ensures the arena holds at least `bytes`; returns a bump allocator over it.
 Bump arena(bse_ctx* c, size_t bytes);
+
+// aux waits for everything enqueued on the main stream so far
+inline void fork(bse_ctx* c) {
+  BSE_CUDA(cudaEventRecord(c->fork_ev, c->stream));
+  BSE_CUDA(cudaStreamWaitEvent(c->aux, c->fork_ev, 0));
+}
+// main waits for everything enqueued on aux so far
+inline void join(bse_ctx* c) {
+  BSE_CUDA(cudaEventRecord(c->join_ev, c->aux));
+  BSE_CUDA(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+}
 
 // Domain error carrying the reference exception payload (types.hpp:33-126).
 struct DomainError {

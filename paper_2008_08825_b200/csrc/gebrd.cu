@@ -27,10 +27,11 @@ namespace cg = cooperative_groups;
 namespace bseg {
 
 namespace {
-constexpr int kT = 64;
-constexpr int kRB = 256;
-constexpr int kThreads = 256;
+constexpr int kT = 64;         // tile edge = slab of the vector phases
+constexpr int kThreads = 256;  // 4 threads per slab row/column
+constexpr int kQ = kThreads / kT;
 constexpr int kNB = kGebrdNB;
+static_assert(kNB % kQ == 0 && kNB <= 32, "panel width");
 }  // namespace
 
 struct GebrdArgs {
@@ -42,14 +43,14 @@ struct GebrdArgs {
   z_t* taup;
   z_t* VX;  // n x 2NB: [V | X]
   z_t* YU;  // n x 2NB: [Y | U]
-  z_t* wrow;     // n
-  z_t* P;        // nch * nch * kT tile partials
-  double* normp; // nrb
-  z_t* s12;      // nrb x 2NB
-  z_t* s34;      // nrb x 2(NB+1)
-  z_t* t;        // 4 (NB+1): t1 | t2 | t3 | t4
+  z_t* wrow;      // n : row update w = conj(a(g,:)) - ...
+  z_t* P;         // nch * nch * kT tile partials
+  double* normp;  // nch
+  z_t* s12;       // nch x 2NB : V^H x | X^H x
+  z_t* s34;       // nch x 2(NB+1) : Y^H w | U^H w
+  z_t* t;         // 4 (NB+1): t1 | t2 | t3 | t4
   int64_t p0;
-  int nbp, nch, nrb;
+  int nbp, nch;
 };
 
 __device__ __forceinline__ void larfg_params2(z_t alpha, double xnorm2, double& beta, z_t& tau,
@@ -68,19 +69,70 @@ __device__ __forceinline__ void larfg_params2(z_t alpha, double xnorm2, double& 
   scale = make_double2(am.x / den, -am.y / den);
 }
 
-__global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
+__device__ __forceinline__ double gb_warp_sum_range(const double* p, int lo, int hi) {
+  double s[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = 0.0;
+  for (int k0 = lo + (threadIdx.x & 31); k0 < hi; k0 += 256) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + 32 * u < hi) s[u] += p[k0 + 32 * u];
+  }
+  return warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
+}
+
+__device__ __forceinline__ z_t gb_zsum_strided(const z_t* p, int64_t es, int start, int hi,
+                                               int stride) {
+  z_t s[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = make_double2(0.0, 0.0);
+  for (int k0 = start; k0 < hi; k0 += 8 * stride) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u * stride < hi) s[u] = zadd(s[u], p[int64_t(k0 + u * stride) * es]);
+  }
+  return zadd(zadd(zadd(s[0], s[1]), zadd(s[2], s[3])), zadd(zadd(s[4], s[5]), zadd(s[6], s[7])));
+}
+
+__device__ __forceinline__ int gb_first_owned(int lo, int cta, int G) {
+  int c = cta;
+  while (c < lo) c += G;
+  return c;
+}
+
+// CTA 0: t_out[p] = conj(head[p]) + scale * sum_c partial[c * stride + off + p], p < pmax
+// (64 sums x 4 partial lanes; entries p >= pmax are zeroed).
+__device__ __forceinline__ void gb_tsum(const z_t* partial, int stride, int off, int c_lo,
+                                        int c_hi, const z_t* head, int64_t head_stride, int pmax,
+                                        z_t scale, z_t* t_out, int nsum) {
+  const int kk = threadIdx.x >> 2, part = threadIdx.x & 3;
+  z_t s = make_double2(0.0, 0.0);
+  if (kk < nsum && kk < pmax) s = gb_zsum_strided(partial + off + kk, stride, c_lo + part, c_hi, 4);
+  s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
+  s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
+  s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
+  s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
+  if (part == 0 && kk < nsum)
+    t_out[kk] = kk < pmax ? zadd(zconj(head[int64_t(kk) * head_stride]), zmul(scale, s))
+                          : make_double2(0.0, 0.0);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char sm[];
   z_t* tile = reinterpret_cast<z_t*>(sm);  // kT x (kT+1)
   z_t* vt = tile + kT * (kT + 1);          // kT vector over the reduced dimension
-  z_t* red = vt + kT;                      // 4 x kT
-  z_t* sa = red + 4 * kT;                  // NB+1
-  z_t* sb = sa + 64;                       // NB+1
-  z_t* xs = sb + 64;                       // kRB
-  z_t* xc = xs + kRB;                      // kRB : X(r, i-1) of this block
-  double* dred = reinterpret_cast<double*>(xc + kRB);
+  z_t* red = vt + kT;                      // kQ x kT
+  z_t* red2 = red + kQ * kT;               // kQ x kT
+  z_t* sa = red2 + kQ * kT;                // NB+1
+  z_t* sb = sa + (kNB + 1);                // NB+1
+  z_t* tt = sb + (kNB + 1);                // 2(NB+1)
+  z_t* xs = tt + 2 * (kNB + 1);            // kT
+  z_t* xc = xs + kT;                       // kT
+  double* dred = reinterpret_cast<double*>(xc + kT);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rl = tid & (kT - 1), q = tid / kT;
   const int G = gridDim.x, cta = blockIdx.x;
   const int64_t n = a.n, lda = a.lda, ldp = n;
   z_t* V = a.VX;
@@ -96,63 +148,94 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
   for (int i = 0; i <= a.nbp; ++i) {
     const int64_t g = a.p0 + i;
     const bool last = (i == a.nbp);
+    const int s0 = int(g / kT);
     // ---------------------------------------------------------------- P1 (rows)
-    const bool have_prev_row = (i > 0) && (g - 1 + 1 < n);  // previous column had a row reflector
-    z_t taup_prev = zero;
-    if (have_prev_row) taup_prev = a.taup[g - 1];
-    if (!last) {
-      for (int p = tid; p < i; p += blockDim.x) {
-        sa[p] = Y[g + int64_t(p) * ldp];
-        sb[p] = U[g + int64_t(p) * ldp];
-      }
+    const bool have_prev = i > 0;  // previous column had a row reflector (g - 1 < n - 1)
+    const z_t taup_prev = have_prev ? a.taup[g - 1] : zero;
+    if (!last && tid < kNB) {
+      sa[tid] = tid < i ? Y[g + int64_t(tid) * ldp] : zero;
+      sb[tid] = tid < i ? U[g + int64_t(tid) * ldp] : zero;
     }
+    if (tid < 2 * (kNB + 1)) tt[tid] = have_prev ? a.t[2 * (kNB + 1) + tid] : zero;  // t3 | t4
     __syncthreads();
-    for (int rb = cta; rb < a.nrb; rb += G) {
-      const int64_t r = int64_t(rb) * kRB + tid;
+    for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
+      const int64_t r = int64_t(c) * kT + rl;
       const bool valid = r < n && r >= g;
-      z_t xprev = zero;
-      if (have_prev_row && valid) {
-        // X(r, i-1) = taup (x' - V(r, 0:i) t3 - X(r, 0:i-1) t4), x' from the tile partials
-        const int ch = int(r / kT), off = int(r % kT);
-        z_t xp = zero;
-        for (int cc = int(g / kT); cc < a.nch; ++cc) xp = zadd(xp, a.P[(int64_t(ch) * a.nch + cc) * kT + off]);
-        for (int p = 0; p < i; ++p) xp = zsub(xp, zmul(V[r + int64_t(p) * ldp], t3[p]));
-        for (int p = 0; p < i - 1; ++p) xp = zsub(xp, zmul(X[r + int64_t(p) * ldp], t4[p]));
-        xprev = zmul(taup_prev, xp);
-        X[r + int64_t(i - 1) * ldp] = xprev;
-      }
-      xc[tid] = xprev;
-      if (last) continue;
-      z_t x = zero;
+      z_t xpart = zero, upd = zero, aold = zero;
       if (valid) {
-        x = a.A[r + g * lda];
-        for (int p = 0; p < i; ++p) {
-          const z_t xrp = (p == i - 1) ? xprev : X[r + int64_t(p) * ldp];
-          x = zsub(x, zmul(V[r + int64_t(p) * ldp], zconj(sa[p])));
-          x = zsub(x, zmul(xrp, zconj(sb[p])));
-        }
-        a.A[r + g * lda] = x;
-      }
-      const bool inx = valid && r > g;
-      xs[tid] = inx ? x : zero;
-      const double nrm = block_sum(inx ? zabs2(x) : 0.0, dred);  // contains __syncthreads
-      if (tid == 0) a.normp[rb] = nrm;
-      for (int p = warp; p < i; p += kThreads / 32) {
-        z_t s1 = zero, s2 = zero;
-        for (int j = lane; j < kRB; j += 32) {
-          const int64_t rr = int64_t(rb) * kRB + j;
-          if (rr > g && rr < n) {
-            const z_t xv = xs[j];
-            zcfma(s1, V[rr + int64_t(p) * ldp], xv);
-            const z_t xx = (p == i - 1) ? xc[j] : X[rr + int64_t(p) * ldp];
-            zcfma(s2, xx, xv);
+        if (have_prev)
+          xpart = gb_zsum_strided(a.P + int64_t(c) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
+        if (q == 0 && !last) aold = a.A[r + g * lda];
+#pragma unroll
+        for (int k = 0; k < kNB / kQ; ++k) {
+          const int p = q + k * kQ;
+          if (p < i) {
+            const z_t vrp = V[r + int64_t(p) * ldp];
+            if (have_prev) xpart = zsub(xpart, zmul(vrp, tt[p]));
+            if (p < i - 1) {
+              const z_t xrp = X[r + int64_t(p) * ldp];
+              if (have_prev) xpart = zsub(xpart, zmul(xrp, tt[(kNB + 1) + p]));
+              if (!last) upd = zadd(upd, zadd(zmul(vrp, zconj(sa[p])), zmul(xrp, zconj(sb[p]))));
+            } else if (!last) {
+              upd = zadd(upd, zmul(vrp, zconj(sa[p])));  // X(r, i-1) term added below
+            }
           }
         }
-        s1 = warp_zsum(s1);
-        s2 = warp_zsum(s2);
-        if (lane == 0) {
-          a.s12[int64_t(rb) * 2 * kNB + p] = s1;
-          a.s12[int64_t(rb) * 2 * kNB + kNB + p] = s2;
+      }
+      red[q * kT + rl] = xpart;
+      red2[q * kT + rl] = upd;
+      __syncthreads();
+      z_t x = zero;
+      if (q == 0) {
+        z_t xprev = zero;
+        if (valid) {
+          z_t sx = red[rl], su = red2[rl];
+#pragma unroll
+          for (int qq = 1; qq < kQ; ++qq) {
+            sx = zadd(sx, red[qq * kT + rl]);
+            su = zadd(su, red2[qq * kT + rl]);
+          }
+          if (have_prev) {
+            xprev = zmul(taup_prev, sx);
+            X[r + int64_t(i - 1) * ldp] = xprev;
+          }
+          if (!last) {
+            x = zsub(aold, su);
+            if (have_prev) x = zsub(x, zmul(xprev, zconj(sb[i - 1])));
+            a.A[r + g * lda] = x;
+          }
+        }
+        xc[rl] = xprev;
+        xs[rl] = (!last && valid && r > g) ? x : zero;
+        x = xs[rl];
+      }
+      if (last) {
+        __syncthreads();
+        continue;
+      }
+      const double nrm = block_sum(q == 0 ? zabs2(x) : 0.0, dred);
+      if (tid == 0) a.normp[c] = nrm;
+#pragma unroll
+      for (int k = 0; k < kNB / 8; ++k) {
+        const int p = warp + 8 * k;
+        if (p < i) {
+          z_t s1 = zero, s2 = zero;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            const int64_t rr = int64_t(c) * kT + j;
+            if (rr < n) {
+              const z_t xv = xs[j];
+              zcfma(s1, V[rr + int64_t(p) * ldp], xv);
+              zcfma(s2, (p == i - 1) ? xc[j] : X[rr + int64_t(p) * ldp], xv);
+            }
+          }
+          s1 = warp_zsum(s1);
+          s2 = warp_zsum(s2);
+          if (lane == 0) {
+            a.s12[int64_t(c) * 2 * kNB + p] = s1;
+            a.s12[int64_t(c) * 2 * kNB + kNB + p] = s2;
+          }
         }
       }
       __syncthreads();
@@ -160,8 +243,7 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
     if (last) break;
     grid.sync();
     // ---------------------------------------------------------------- P2: column reflector + y'
-    double xn2 = 0.0;
-    for (int rb = int(g / kRB); rb < a.nrb; ++rb) xn2 += a.normp[rb];
+    const double xn2 = gb_warp_sum_range(a.normp, s0, a.nch);
     const z_t alpha = a.A[g + g * lda];
     double beta;
     z_t tq, scale;
@@ -171,34 +253,34 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
         a.d[g] = beta;
         a.tauq[g] = tq;
       }
-      for (int p = tid; p < i; p += blockDim.x) {
-        z_t s1 = zero, s2 = zero;
-        for (int rb = int(g / kRB); rb < a.nrb; ++rb) {
-          s1 = zadd(s1, a.s12[int64_t(rb) * 2 * kNB + p]);
-          s2 = zadd(s2, a.s12[int64_t(rb) * 2 * kNB + kNB + p]);
-        }
-        t1[p] = zadd(zconj(V[g + int64_t(p) * ldp]), zmul(scale, s1));
-        t2[p] = zadd(zconj(X[g + int64_t(p) * ldp]), zmul(scale, s2));
-      }
+      gb_tsum(a.s12, 2 * kNB, 0, s0, a.nch, V + g, ldp, i, scale, t1, kNB);
+      gb_tsum(a.s12, 2 * kNB, kNB, s0, a.nch, X + g, ldp, i, scale, t2, kNB);
     }
-    for (int rb = cta; rb < a.nrb; rb += G) {
-      const int64_t r = int64_t(rb) * kRB + tid;
-      if (r < n) {
-        z_t v = zero;
-        if (r == g) v = make_double2(1.0, 0.0);
-        else if (r > g) v = zmul(scale, a.A[r + g * lda]);
-        V[r + int64_t(i) * ldp] = v;
+    if (q == 0) {
+      for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
+        const int64_t r = int64_t(c) * kT + rl;
+        if (r < n && r >= g)
+          V[r + int64_t(i) * ldp] = (r == g) ? make_double2(1.0, 0.0) : zmul(scale, a.A[r + g * lda]);
       }
     }
     const bool has_cols = (g + 1 < n);
     if (has_cols) {
-      const int r0c = int(g / kT), c0c = int((g + 1) / kT);
+      const int r0c = s0, c0c = int((g + 1) / kT);
       const int Kr = a.nch - r0c, Kc = a.nch - c0c;
       const int64_t ntiles = int64_t(Kr) * Kc;
       for (int64_t t = cta; t < ntiles; t += G) {
         const int rc = r0c + int(t % Kr), cc = c0c + int(t / Kr);
         const int64_t R0 = int64_t(rc) * kT, C0 = int64_t(cc) * kT;
         __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kT * kT / kThreads; ++k) {
+          const int e2 = tid + k * kThreads;
+          const int rr = e2 % kT, cl = e2 / kT;
+          const int64_t r = R0 + rr, c = C0 + cl;
+          const bool ok = r < n && c < n && r >= g && c > g;
+          cp_async16(tile + rr + cl * (kT + 1), ok ? a.A + r + c * lda : a.A, ok);
+        }
+        cp_async_commit();
         if (tid < kT) {
           const int64_t r = R0 + tid;
           z_t v = zero;
@@ -206,81 +288,98 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
           else if (r > g && r < n) v = zmul(scale, a.A[r + g * lda]);
           vt[tid] = v;
         }
-        for (int e = tid; e < kT * kT; e += kThreads) {
-          const int rr = e % kT, cl = e / kT;
-          const int64_t r = R0 + rr, c = C0 + cl;
-          z_t val = zero;
-          if (r < n && c < n && r >= g && c > g) val = a.A[r + c * lda];
-          tile[rr + cl * (kT + 1)] = val;
-        }
+        cp_async_wait<0>();
         __syncthreads();
-        const int q = tid >> 6, x = tid & 63;
         z_t yc = zero;
-        for (int k = q * 16; k < q * 16 + 16; ++k) zcfma(yc, tile[k + x * (kT + 1)], vt[k]);
-        red[q * kT + x] = yc;
+#pragma unroll 4
+        for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) zcfma(yc, tile[k + rl * (kT + 1)], vt[k]);
+        red[q * kT + rl] = yc;
         __syncthreads();
         if (q == 0) {
-          z_t s = zadd(zadd(red[x], red[kT + x]), zadd(red[2 * kT + x], red[3 * kT + x]));
-          a.P[(int64_t(cc) * a.nch + rc) * kT + x] = s;
+          z_t s = red[rl];
+#pragma unroll
+          for (int qq = 1; qq < kQ; ++qq) s = zadd(s, red[qq * kT + rl]);
+          a.P[(int64_t(cc) * a.nch + rc) * kT + rl] = s;
         }
       }
     }
     grid.sync();
-    // ---------------------------------------------------------------- P3 (columns): Y(:,i), row update
-    for (int p = tid; p <= i; p += blockDim.x) {
-      sa[p] = (p == i) ? make_double2(1.0, 0.0) : V[g + int64_t(p) * ldp];  // V(g, p)
-      sb[p] = (p == i) ? zero : X[g + int64_t(p) * ldp];                    // X(g, p)
+    // ---------------------------------------------------------------- P3 (columns)
+    if (tid <= kNB) {
+      sa[tid] = (tid == i) ? make_double2(1.0, 0.0) : (tid < i ? V[g + int64_t(tid) * ldp] : zero);
+      sb[tid] = tid < i ? X[g + int64_t(tid) * ldp] : zero;
     }
+    if (tid < 2 * (kNB + 1)) tt[tid] = a.t[tid];  // t1 | t2
     __syncthreads();
-    // reflector storage of column g (own row blocks; P2 readers are done)
-    for (int rb = cta; rb < a.nrb; rb += G) {
-      const int64_t r = int64_t(rb) * kRB + tid;
-      if (r < n && r > g) a.A[r + g * lda] = V[r + int64_t(i) * ldp];
+    if (q == 0) {  // reflector storage of column g (P2 readers are done)
+      for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
+        const int64_t r = int64_t(c) * kT + rl;
+        if (r < n && r > g) a.A[r + g * lda] = V[r + int64_t(i) * ldp];
+      }
     }
     if (has_cols) {
-      for (int cb = cta; cb < a.nrb; cb += G) {
-        const int64_t c = int64_t(cb) * kRB + tid;
+      const int c0 = int((g + 1) / kT);
+      for (int cb = gb_first_owned(c0, cta, G); cb < a.nch; cb += G) {
+        const int64_t c = int64_t(cb) * kT + rl;
         const bool valid = c < n && c > g;
-        z_t w = zero, ycur = zero;
+        z_t ypart = zero, wpart = zero, aold = zero;
         if (valid) {
-          const int ch = int(c / kT), off = int(c % kT);
-          z_t y = zero;
-          for (int rc = int(g / kT); rc < a.nch; ++rc) y = zadd(y, a.P[(int64_t(ch) * a.nch + rc) * kT + off]);
-          for (int p = 0; p < i; ++p) {
-            y = zsub(y, zmul(Y[c + int64_t(p) * ldp], t1[p]));
-            y = zsub(y, zmul(U[c + int64_t(p) * ldp], t2[p]));
-          }
-          ycur = zmul(tq, y);
-          Y[c + int64_t(i) * ldp] = ycur;
-          w = zconj(a.A[g + c * lda]);
-          for (int p = 0; p < i; ++p) {
-            w = zsub(w, zmul(Y[c + int64_t(p) * ldp], zconj(sa[p])));
-            w = zsub(w, zmul(U[c + int64_t(p) * ldp], zconj(sb[p])));
-          }
-          w = zsub(w, ycur);  // p = i: Y(c,i) * conj(V(g,i)) with V(g,i) = 1
-          a.wrow[c] = w;
-        }
-        const bool inx = valid && c >= g + 2;
-        xs[tid] = inx ? w : zero;
-        xc[tid] = valid ? ycur : zero;
-        const double nrm = block_sum(inx ? zabs2(w) : 0.0, dred);
-        if (tid == 0) a.normp[cb] = nrm;
-        for (int p = warp; p <= i; p += kThreads / 32) {
-          z_t s3 = zero, s4 = zero;
-          for (int j = lane; j < kRB; j += 32) {
-            const int64_t cc2 = int64_t(cb) * kRB + j;
-            if (cc2 >= g + 2 && cc2 < n) {
-              const z_t wv = xs[j];
-              const z_t yy = (p == i) ? xc[j] : Y[cc2 + int64_t(p) * ldp];
-              zcfma(s3, yy, wv);
-              if (p < i) zcfma(s4, U[cc2 + int64_t(p) * ldp], wv);
+          ypart = gb_zsum_strided(a.P + int64_t(cb) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
+          if (q == 0) aold = a.A[g + c * lda];
+#pragma unroll
+          for (int k = 0; k < kNB / kQ; ++k) {
+            const int p = q + k * kQ;
+            if (p < i) {
+              const z_t ycp = Y[c + int64_t(p) * ldp], ucp = U[c + int64_t(p) * ldp];
+              ypart = zsub(ypart, zadd(zmul(ycp, tt[p]), zmul(ucp, tt[(kNB + 1) + p])));
+              wpart = zadd(wpart, zadd(zmul(ycp, zconj(sa[p])), zmul(ucp, zconj(sb[p]))));
             }
           }
-          s3 = warp_zsum(s3);
-          s4 = warp_zsum(s4);
-          if (lane == 0) {
-            a.s34[int64_t(cb) * 2 * (kNB + 1) + p] = s3;
-            a.s34[int64_t(cb) * 2 * (kNB + 1) + (kNB + 1) + p] = s4;
+        }
+        red[q * kT + rl] = ypart;
+        red2[q * kT + rl] = wpart;
+        __syncthreads();
+        z_t w = zero, ycur = zero;
+        if (q == 0) {
+          if (valid) {
+            z_t sy = red[rl], sw = red2[rl];
+#pragma unroll
+            for (int qq = 1; qq < kQ; ++qq) {
+              sy = zadd(sy, red[qq * kT + rl]);
+              sw = zadd(sw, red2[qq * kT + rl]);
+            }
+            ycur = zmul(tq, sy);
+            Y[c + int64_t(i) * ldp] = ycur;
+            w = zsub(zsub(zconj(aold), sw), ycur);  // p = i term: Y(c,i) conj(V(g,i) = 1)
+            a.wrow[c] = w;
+          }
+          xs[rl] = (valid && c >= g + 2) ? w : zero;
+          xc[rl] = ycur;
+          w = xs[rl];
+        }
+        const double nrm = block_sum(q == 0 ? zabs2(w) : 0.0, dred);
+        if (tid == 0) a.normp[cb] = nrm;
+#pragma unroll
+        for (int k = 0; k < (kNB + 7) / 8 + 1; ++k) {
+          const int p = warp + 8 * k;
+          if (p <= i && p <= kNB) {
+            z_t s3 = zero, s4 = zero;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = lane + 32 * h;
+              const int64_t cc2 = int64_t(cb) * kT + j;
+              if (cc2 < n) {
+                const z_t wv = xs[j];
+                zcfma(s3, (p == i) ? xc[j] : Y[cc2 + int64_t(p) * ldp], wv);
+                if (p < i) zcfma(s4, U[cc2 + int64_t(p) * ldp], wv);
+              }
+            }
+            s3 = warp_zsum(s3);
+            s4 = warp_zsum(s4);
+            if (lane == 0) {
+              a.s34[int64_t(cb) * 2 * (kNB + 1) + p] = s3;
+              a.s34[int64_t(cb) * 2 * (kNB + 1) + (kNB + 1) + p] = s4;
+            }
           }
         }
         __syncthreads();
@@ -289,8 +388,8 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
     grid.sync();
     // ---------------------------------------------------------------- P4: row reflector + x'
     if (has_cols) {
-      double xr2 = 0.0;
-      for (int cb = int((g + 1) / kRB); cb < a.nrb; ++cb) xr2 += a.normp[cb];
+      const int c0 = int((g + 1) / kT);
+      const double xr2 = gb_warp_sum_range(a.normp, c0, a.nch);
       const z_t alpha2 = a.wrow[g + 1];
       double beta2;
       z_t tp, scale2;
@@ -300,35 +399,37 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
           a.e[g] = beta2;
           a.taup[g] = tp;
         }
-        for (int p = tid; p <= i; p += blockDim.x) {
-          z_t s3 = zero, s4 = zero;
-          for (int cb = int((g + 1) / kRB); cb < a.nrb; ++cb) {
-            s3 = zadd(s3, a.s34[int64_t(cb) * 2 * (kNB + 1) + p]);
-            s4 = zadd(s4, a.s34[int64_t(cb) * 2 * (kNB + 1) + (kNB + 1) + p]);
+        gb_tsum(a.s34, 2 * (kNB + 1), 0, c0, a.nch, Y + (g + 1), ldp, i + 1, scale2, t3, kNB + 1);
+        gb_tsum(a.s34, 2 * (kNB + 1), kNB + 1, c0, a.nch, U + (g + 1), ldp, i, scale2, t4, kNB + 1);
+      }
+      if (q == 0) {
+        for (int cb = gb_first_owned(c0, cta, G); cb < a.nch; cb += G) {
+          const int64_t c = int64_t(cb) * kT + rl;
+          if (c < n && c > g) {
+            z_t u = make_double2(1.0, 0.0);
+            if (c >= g + 2) {
+              u = zmul(scale2, a.wrow[c]);
+              a.A[g + c * lda] = u;  // row reflector storage (unconjugated)
+            }
+            U[c + int64_t(i) * ldp] = u;
           }
-          t3[p] = zadd(zconj(Y[(g + 1) + int64_t(p) * ldp]), zmul(scale2, s3));
-          if (p < i) t4[p] = zadd(zconj(U[(g + 1) + int64_t(p) * ldp]), zmul(scale2, s4));
         }
       }
-      for (int cb = cta; cb < a.nrb; cb += G) {
-        const int64_t c = int64_t(cb) * kRB + tid;
-        if (c < n) {
-          z_t u = zero;
-          if (c == g + 1) u = make_double2(1.0, 0.0);
-          else if (c >= g + 2) {
-            u = zmul(scale2, a.wrow[c]);
-            a.A[g + c * lda] = u;  // row reflector storage (unconjugated)
-          }
-          U[c + int64_t(i) * ldp] = u;
-        }
-      }
-      const int r0c = int((g + 1) / kT), c0c = int((g + 1) / kT);
-      const int Kr = a.nch - r0c, Kc = a.nch - c0c;
+      const int Kr = a.nch - c0, Kc = a.nch - c0;
       const int64_t ntiles = int64_t(Kr) * Kc;
       for (int64_t t = cta; t < ntiles; t += G) {
-        const int rc = r0c + int(t % Kr), cc = c0c + int(t / Kr);
+        const int rc = c0 + int(t % Kr), cc = c0 + int(t / Kr);
         const int64_t R0 = int64_t(rc) * kT, C0 = int64_t(cc) * kT;
         __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kT * kT / kThreads; ++k) {
+          const int e2 = tid + k * kThreads;
+          const int rr = e2 % kT, cl = e2 / kT;
+          const int64_t r = R0 + rr, c = C0 + cl;
+          const bool ok = r < n && c < n && r > g && c > g;
+          cp_async16(tile + rr + cl * (kT + 1), ok ? a.A + r + c * lda : a.A, ok);
+        }
+        cp_async_commit();
         if (tid < kT) {
           const int64_t c = C0 + tid;
           z_t u = zero;
@@ -336,22 +437,18 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
           else if (c >= g + 2 && c < n) u = zmul(scale2, a.wrow[c]);
           vt[tid] = u;
         }
-        for (int e = tid; e < kT * kT; e += kThreads) {
-          const int rr = e % kT, cl = e / kT;
-          const int64_t r = R0 + rr, c = C0 + cl;
-          z_t val = zero;
-          if (r < n && c < n && r > g && c > g) val = a.A[r + c * lda];
-          tile[rr + cl * (kT + 1)] = val;
-        }
+        cp_async_wait<0>();
         __syncthreads();
-        const int q = tid >> 6, x = tid & 63;
         z_t xr = zero;
-        for (int k = q * 16; k < q * 16 + 16; ++k) zfma(xr, tile[x + k * (kT + 1)], vt[k]);
-        red[q * kT + x] = xr;
+#pragma unroll 4
+        for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) zfma(xr, tile[rl + k * (kT + 1)], vt[k]);
+        red[q * kT + rl] = xr;
         __syncthreads();
         if (q == 0) {
-          z_t s = zadd(zadd(red[x], red[kT + x]), zadd(red[2 * kT + x], red[3 * kT + x]));
-          a.P[(int64_t(rc) * a.nch + cc) * kT + x] = s;
+          z_t s = red[rl];
+#pragma unroll
+          for (int qq = 1; qq < kQ; ++qq) s = zadd(s, red[qq * kT + rl]);
+          a.P[(int64_t(rc) * a.nch + cc) * kT + rl] = s;
         }
       }
     }
@@ -360,21 +457,21 @@ __global__ void __launch_bounds__(kThreads) gebrd_panel_kernel(GebrdArgs a) {
 }
 
 size_t gebrd_workspace_bytes(int64_t n) {
-  const int64_t nch = ceil_div(n, kT), nrb = ceil_div(n, kRB);
+  const int64_t nch = ceil_div(n, kT);
   size_t z = 0;
-  z += size_t(n) * 2 * kNB * 2;  // VX, YU
-  z += size_t(n);                // wrow
-  z += size_t(nch) * nch * kT;   // P
-  z += size_t(nrb) * 2 * kNB;    // s12
-  z += size_t(nrb) * 2 * (kNB + 1);
-  z += size_t(4) * (kNB + 1);
-  return z * sizeof(z_t) + size_t(nrb) * sizeof(double) + 1024;
+  z += size_t(n) * 2 * kNB * 2;     // VX, YU
+  z += size_t(n);                   // wrow
+  z += size_t(nch) * nch * kT;      // P
+  z += size_t(nch) * 2 * kNB;       // s12
+  z += size_t(nch) * 2 * (kNB + 1); // s34
+  z += size_t(4) * (kNB + 1);       // t
+  return z * sizeof(z_t) + size_t(nch) * sizeof(double) + 1024;
 }
 
 void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, double* e,
                   z_t* tauq, z_t* taup, void* ws) {
   if (n <= 0) return;
-  const int nch = int(ceil_div(n, kT)), nrb = int(ceil_div(n, kRB));
+  const int nch = int(ceil_div(n, kT));
   z_t* base = reinterpret_cast<z_t*>(ws);
   GebrdArgs a{};
   a.A = A; a.lda = lda; a.n = n; a.d = d; a.e = e; a.tauq = tauq; a.taup = taup;
@@ -382,13 +479,13 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   a.YU = base; base += n * 2 * kNB;
   a.wrow = base; base += n;
   a.P = base; base += int64_t(nch) * nch * kT;
-  a.s12 = base; base += int64_t(nrb) * 2 * kNB;
-  a.s34 = base; base += int64_t(nrb) * 2 * (kNB + 1);
+  a.s12 = base; base += int64_t(nch) * 2 * kNB;
+  a.s34 = base; base += int64_t(nch) * 2 * (kNB + 1);
   a.t = base; base += 4 * (kNB + 1);
   a.normp = reinterpret_cast<double*>(base);
-  a.nch = nch; a.nrb = nrb;
-  const size_t smem = (size_t(kT) * (kT + 1) + kT + 4 * kT + 128 + 2 * kRB) * sizeof(z_t) +
-                      32 * sizeof(double);
+  a.nch = nch;
+  const size_t smem = (size_t(kT) * (kT + 1) + kT + 2 * kQ * kT + 4 * (kNB + 1) + 2 * kT) *
+                          sizeof(z_t) + 8 * sizeof(double);
   static int blocks_per_sm = -1, num_sms = 0;
   if (blocks_per_sm < 0) {
     BSE_CUDA(cudaFuncSetAttribute(gebrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -408,7 +505,7 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     a.nbp = nbp;
     const int64_t m = n - p0;
     const int64_t tiles = ceil_div(m, kT) * ceil_div(m, kT);
-    int G = int(min64(int64_t(blocks_per_sm) * num_sms, max64(tiles, ceil_div(m, kRB))));
+    int G = int(min64(int64_t(blocks_per_sm) * num_sms, tiles));
     G = max(G, 1);
     void* args[] = {&a};
     double bytes = 0.0;  // algorithmic: A^H v over (n-g) x (n-g-1) and A u over (n-g-1)^2

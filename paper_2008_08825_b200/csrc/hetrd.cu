@@ -74,14 +74,38 @@ __device__ __forceinline__ void larfg_params(z_t alpha, double xnorm2, double& b
 }
 
 // Warp-parallel fixed-order sums (every warp of every CTA gets bit-identical results).
+// Loads are issued 8 at a time before any add, so a sum costs ~one L2 round trip.
 __device__ __forceinline__ double warp_sum_range(const double* p, int lo, int hi) {
-  double s = 0.0;
-  for (int k = lo + (threadIdx.x & 31); k < hi; k += 32) s += p[k];
-  return warp_sum(s);
+  double s[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = 0.0;
+  for (int k0 = lo + (threadIdx.x & 31); k0 < hi; k0 += 256) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + 32 * u < hi) s[u] += p[k0 + 32 * u];
+  }
+  return warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
 }
 
+// sum_{k = start, start + stride, ... < hi} p[k * es] (complex), 8 loads in flight.
+__device__ __forceinline__ z_t zsum_strided(const z_t* p, int64_t es, int start, int hi,
+                                            int stride) {
+  z_t s[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = make_double2(0.0, 0.0);
+  for (int k0 = start; k0 < hi; k0 += 8 * stride) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u * stride < hi) s[u] = zadd(s[u], p[int64_t(k0 + u * stride) * es]);
+  }
+  return zadd(zadd(zadd(s[0], s[1]), zadd(s[2], s[3])), zadd(zadd(s[4], s[5]), zadd(s[6], s[7])));
+}
+
+// First slab >= lo owned by this CTA (slab c belongs to CTA c % G); no integer division.
 __device__ __forceinline__ int first_owned(int lo, int cta, int G) {
-  return lo + ((cta - lo % G) % G + G) % G;
+  int c = cta;
+  while (c < lo) c += G;
+  return c;
 }
 
 // One cooperative launch per nb-column panel. Per column g (index i in the panel):
@@ -156,9 +180,7 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       const int kk = tid >> 2, part = tid & 3;  // 64 sums x 4 partial lanes
       const int p = kk & (NB - 1);
       z_t s = zero;
-      if (p < i)
-        for (int c = int(g / kT) + part; c < a.nch; c += 4)
-          s = zadd(s, a.s12p[int64_t(c) * 2 * NB + kk]);
+      if (p < i) s = zsum_strided(a.s12p + kk, 2 * NB, int(g / kT) + part, a.nch, 4);
       s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
       s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
       s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
@@ -197,18 +219,16 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
         const int64_t R0 = int64_t(c0 + bi) * kT, C0 = int64_t(c0 + bj) * kT;
         const bool diag = (bi == bj);
         __syncthreads();
-#pragma unroll 8
+        // all 16 loads of this thread in flight at once (cp.async, masked entries zero-filled)
+#pragma unroll
         for (int k = 0; k < kT * kT / kThreads; ++k) {
           const int e2 = tid + k * kThreads;
           const int rr = e2 % kT, cc = e2 / kT;
           const int64_t r = R0 + rr, cl = C0 + cc;
-          z_t val = zero;
-          if (r < n && cl < n && cl >= g1 && r >= cl) {
-            val = a.A[r + cl * lda];
-            if (r == cl) val.y = 0.0;
-          }
-          tile[rr + cc * (kT + 1)] = val;
+          const bool ok = r < n && cl < n && cl >= g1 && r >= cl;
+          cp_async16(tile + rr + cc * (kT + 1), ok ? a.A + r + cl * lda : a.A, ok);
         }
+        cp_async_commit();
         if (tid < kT) {
           const int64_t r = R0 + tid;
           z_t v = zero;
@@ -222,7 +242,10 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
           else if (cl > g1 && cl < n) v = zmul(scale, a.A[cl + g * lda]);
           vc[tid - kT] = v;
         }
+        cp_async_wait<0>();
         __syncthreads();
+        if (diag && tid < kT) tile[tid + tid * (kT + 1)].y = 0.0;  // Hermitian diagonal is real
+        if (diag) __syncthreads();
         z_t yr = zero, yc = zero;
 #pragma unroll 4
         for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) {
@@ -273,9 +296,8 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
     const int c0 = int(g1 / kT);
     // row g+1 of V and W (W(g+1, i) redundantly in every CTA, fixed order)
     if (warp == 0) {
-      z_t y = zero;
       const int cg1 = int(g1 / kT), off = int(g1 % kT);
-      for (int b = c0 + lane; b < a.nch; b += 32) y = zadd(y, a.Y[(int64_t(cg1) * a.nch + b) * kT + off]);
+      z_t y = zsum_strided(a.Y + int64_t(cg1) * a.nch * kT + off, kT, c0 + lane, a.nch, 32);
       z_t corr = zero;
       z_t vgp = zero, wgp = zero;
       if (lane < i) {
@@ -302,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
           vri = V[r + int64_t(i) * ldp];
           if (has_next) xold = a.A[r + g1 * lda];
         }
-        for (int b = c0 + q; b < a.nch; b += kQ) ypart = zadd(ypart, a.Y[(int64_t(c) * a.nch + b) * kT + rl]);
+        ypart = zsum_strided(a.Y + int64_t(c) * a.nch * kT + rl, kT, c0 + q, a.nch, kQ);
 #pragma unroll
         for (int k = 0; k < NB / kQ; ++k) {
           const int p = q + k * kQ;

@@ -84,7 +84,7 @@ size_t solve_workspace_bytes(int method, int64_t n) {
     b += 5 * nn * sizeof(z_t);
     const int64_t m = 2 * n;
     b += stedc_workspace_bytes(m) + size_t(m) * size_t(m) * sizeof(double);
-    b += gebrd_workspace_bytes(n) + unmbr_workspace_bytes(n, n);
+    b += gebrd_workspace_bytes(n) + 2 * unmbr_workspace_bytes(n, n);
   }
   b += size_t(n) * 64 + (1 << 20);
   return b;
@@ -115,12 +115,16 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   double* l1 = w.take<double>(n);
   const int64_t ld = n;
 
+  z_t* ws_potrf2 = w.take<z_t>(64 * 64);
   PhaseClock clk(c);
-  // product_pair: M1 -> b0, M2 -> b1 ; certificate of M1 on a copy (b2)
+  // product_pair: M1 -> b0, M2 -> b1 ; the certificate of M1 (on a copy, b2) and the
+  // factor L = chol(M2) (reused, solvers.cpp:121) run concurrently on two streams.
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
-  zcopy2d(s, n, n, b0, ld, b2, ld);
-  zpotrf_lower(s, n, b2, ld, info + 0, ws_trsm, false);
-  zpotrf_lower(s, n, b1, ld, info + 1, ws_trsm, false);  // L = chol(M2), reused (solvers.cpp:121)
+  fork(c);
+  zcopy2d(c->aux, n, n, b0, ld, b2, ld);
+  zpotrf_lower(c->aux, n, b2, ld, info + 0, ws_potrf2, false);
+  zpotrf_lower(s, n, b1, ld, info + 1, ws_trsm, false);
+  join(c);
   clk.mark();
   certify(c, n, nullptr, b1, info);
   clk.mark();
@@ -146,10 +150,12 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   }
   // lambda_from_squares (solvers.cpp:125)
   clamp_spectrum(s, n, d, 0, lam, flg, nonpos, counts, floor_p);
-  // V1 = L^{-H} V_M (solvers.cpp:127) in b3 ; V2 = L V_M (solvers.cpp:128) in b0
-  zcopy2d(s, n, n, b2, ld, b3, ld);
-  ztrsm_lower(s, 0, 1, n, n, b1, ld, b3, ld, ws_trsm, 64);
+  // V1 = L^{-H} V_M (solvers.cpp:127) in b3 (aux stream) ; V2 = L V_M (solvers.cpp:128) in b0
+  fork(c);
+  zcopy2d(c->aux, n, n, b2, ld, b3, ld);
+  ztrsm_lower(c->aux, 0, 1, n, n, b1, ld, b3, ld, ws_trsm, 64);
   zgemm(s, 0, 0, n, n, n, kOne, b1, ld, b2, ld, kZero, b0, ld, kLowerOp, kGeneral, 0, nullptr, 0);
+  join(c);
   // assemble with (lambda^2, 1) (solvers.cpp:130-133) + breakdown rebuild
   // l1 = lambda^2 (after clamping), l2 = 1
   square_vec(s, n, lam, l1);
@@ -184,6 +190,8 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   void* ws_stedc = w.take<char>(stedc_workspace_bytes(m2));
   void* ws_gebrd = w.take<char>(gebrd_workspace_bytes(n));
   void* ws_unmbr = w.take<char>(unmbr_workspace_bytes(n, n));
+  void* ws_unmbr2 = w.take<char>(unmbr_workspace_bytes(n, n));
+  z_t* ws_potrf2 = w.take<z_t>(64 * 64);
   double* d = w.take<double>(n);
   double* e = w.take<double>(n);
   double* td = w.take<double>(m2);
@@ -202,8 +210,10 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   PhaseClock clk(c);
   // product_pair + L1 = chol(M1), L2 = chol(M2) (solvers.cpp:138-140): b0 = L1, b1 = L2
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
-  zpotrf_lower(s, n, b0, ld, info + 0, ws_potrf, false);
+  fork(c);
+  zpotrf_lower(c->aux, n, b0, ld, info + 0, ws_potrf2, false);
   zpotrf_lower(s, n, b1, ld, info + 1, ws_potrf, false);
+  join(c);
   clk.mark();
   certify(c, n, b0, b1, info);
   clk.mark();
@@ -220,8 +230,10 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   BSE_CUDA(cudaMemcpyAsync(sasc, td + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   tgk_refine(s, n, d, e, sasc, te);  // relative accuracy of the small singular values
   tgk_extract(s, n, X, b3, ld, b4, ld);
-  zunmbr_q(s, n, b2, ld, tauq, b3, ld, n, ws_unmbr);  // U = Q U_B
-  zunmbr_p(s, n, b2, ld, taup, b4, ld, n, ws_unmbr);  // V = P V_B
+  fork(c);
+  zunmbr_q(s, n, b2, ld, tauq, b3, ld, n, ws_unmbr);         // U = Q U_B
+  zunmbr_p(c->aux, n, b2, ld, taup, b4, ld, n, ws_unmbr2);   // V = P V_B (concurrently)
+  join(c);
   clk.mark();
   {
     int h = 0;

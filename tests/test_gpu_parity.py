@@ -302,8 +302,11 @@ def test_breakdown_regime_gpu():
     a, b = configs.generate_conditioned(200, 1e10, 1)
     r = bse.solve_chol_svd(bse.from_blocks(a, b))
     assert sigma_orthogonality_error(r.v) < 1e-8
+    # CHOL far beyond the squaring barrier: finite, clamp contract respected (whether the
+    # garbage smallest squares come out <= eps*d_max depends on rounding)
     rc = bse.solve_chol(bse.from_blocks(a, b))
-    assert np.all(np.isfinite(rc.lambda_)) and np.all(np.isfinite(rc.v)) and rc.near_singular
+    assert np.all(np.isfinite(rc.lambda_)) and np.all(np.isfinite(rc.v))
+    assert np.all(rc.lambda_ >= EPS * rc.lambda_[-1] * (1 - 1e-12))
 
 
 def test_unaccelerated_methods_refuse():
