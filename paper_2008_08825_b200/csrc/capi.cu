@@ -414,6 +414,7 @@ int bse_matmul(bse_ctx* c, int64_t ar, int64_t ac, const double* a, int64_t lda,
     } else {
       zgemm(c->stream, op_a, op_b, am, bn, ak, kOne, dA, ar, dB, br, kZero, dC, am, sa, sb, 0,
             nullptr, 0);
+      collect_timer(c);
     }
     d2h(c, cmat, ldc, dC, am, am, bn);
     BSE_CUDA(cudaStreamSynchronize(c->stream));

@@ -5,18 +5,20 @@
 // proj/src/backend.cpp:34. Same algorithm as LAPACK's zlatrd
 // ('L') panel + zher2k trailing update, re-laid-out for B200:
 //
-//  * One persistent cooperative kernel per nb-column panel. Per column g three grid-wide
-//    phases (separated by grid barriers) replace LAPACK's ~8 BLAS-2 calls:
-//      P1  finalize W(:,g-1); column update a(:,g) -= V W(g,:)^H + W V(g,:)^H; partial
-//          norms and partial V^H x / W^H x products per 256-row block (fixed-order partials,
-//          deterministic);
-//      P2  reflector (zlarfg, recomputed redundantly by every CTA from the partials) and the
-//          Hermitian matrix-vector product y = A22 v over the LOWER triangle only: 64x64
-//          tiles staged in shared memory, each tile contributes A_t v to its row chunk and
-//          A_t^H v to its column chunk (2.67 n^3 bytes total, the HBM-bound half of zhetrd);
-//      P3  reduce the tile partials, w = tau (y - V t1 - W t2), partial dot w^H v.
+//  * One persistent cooperative kernel per nb-column panel. Per column g two grid-wide
+//    phases replace LAPACK's ~8 BLAS-2 calls (see hetrd_panel_kernel):
+//      A  reflector (zlarfg, recomputed redundantly by every CTA from per-slab partial
+//         norms) and the Hermitian matrix-vector product y = A22 v over the LOWER triangle
+//         only: 64x64 tiles (cp.async into shared memory), each contributing A_t v to its
+//         row chunk and A_t^H v to its column chunk (2.67 n^3 bytes over the reduction, the
+//         HBM-bound half of zhetrd), plus per-CTA partials of v^H A22 v;
+//      B  alpha from v^H A v (no extra dot reduction), W(:,g) = tau (y - V t1 - W t2) +
+//         alpha v, and the next column's update with its partial norms / V^H x / W^H x.
+//    All partial sums have a fixed order (bit-deterministic).
 //  * The trailing update A22 -= V W^H + W V^H is one DMMA GEMM with k = 2 nb writing only
 //    lower tiles.
+//  * Back-transformation: all reflector blocks, their T factors and V T products are formed
+//    up front (batched); each 128-reflector block then costs two DMMA GEMMs.
 #include <cooperative_groups.h>
 
 #include "blas.h"
@@ -491,113 +493,110 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
 // Blocks of kBT reflectors, last block first:  Z <- (I - V T V^H) Z  with T from zlarft
 // (forward, columnwise): three DMMA GEMMs + one small triangular kernel per block.
 namespace {
-constexpr int kBT = 64;
+constexpr int kBT = 128;  // reflectors per applied block (the K of the update GEMM)
 }
 
-// Build the reflector block Vb (m x kb, explicit unit and zeros) for reflectors j0..j0+kb-1,
-// covering rows off+j0 .. n-1 (row offset r = row - (j0+off)):
-//   mode 0 (zhetrd 'L', off 1): v_j(j+1) = 1, v_j(r) = A(r, j)  for r > j+1
-//   mode 1 (zgebrd Q,   off 0): v_j(j)   = 1, v_j(r) = A(r, j)  for r > j
-//   mode 2 (zgebrd P,   off 1): u_j(j+1) = 1, u_j(c) = A(j, c)  for c > j+1 (row storage)
-__global__ void build_v_kernel(const z_t* __restrict__ A, int64_t lda, int64_t n, int64_t j0,
-                               int kb, int mode, z_t* __restrict__ Vb, int64_t ldv) {
+// Explicit reflector matrix Vall (n x nblk*kBT, ld n): column j = v_j with explicit unit and
+// zeros (padding columns j >= nref are zero):
+//   mode 0 (zhetrd 'L'): v_j(j+1) = 1, v_j(r) = A(r, j)  for r > j+1
+//   mode 1 (zgebrd Q)  : v_j(j)   = 1, v_j(r) = A(r, j)  for r > j
+//   mode 2 (zgebrd P)  : u_j(j+1) = 1, u_j(c) = A(j, c)  for c > j+1 (row storage)
+__global__ void build_vall_kernel(const z_t* __restrict__ A, int64_t lda, int64_t n,
+                                  int64_t nref, int64_t ncol, int mode, z_t* __restrict__ Vall) {
   const int off = mode == 1 ? 0 : 1;
-  const int64_t m = n - j0 - off;
-  const int64_t total = m * kb;
+  const int64_t total = n * ncol;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = e % m;
-    const int c = int(e / m);
-    const int64_t row = j0 + off + r;  // global row of the reflector vector
-    const int64_t jc = j0 + c;         // reflector index
-    const int64_t unit = jc + off;
+    const int64_t r = e % n, j = e / n;
     z_t v = make_double2(0.0, 0.0);
-    if (row == unit) v = make_double2(1.0, 0.0);
-    else if (row > unit) v = (mode == 2) ? A[jc + row * lda] : A[row + jc * lda];
-    Vb[r + int64_t(c) * ldv] = v;
+    if (j < nref) {
+      const int64_t unit = j + off;
+      if (r == unit) v = make_double2(1.0, 0.0);
+      else if (r > unit) v = (mode == 2) ? A[j + r * lda] : A[r + j * lda];
+    }
+    Vall[e] = v;
   }
 }
 
-// T (kb x kb upper) from the Gram matrix G = V^H V (kb x kb) and tau:
-// T(i,i) = tau_i ; T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i).
-__global__ void larft_kernel(const z_t* __restrict__ Gm, int kb, const z_t* __restrict__ tau,
-                             z_t* __restrict__ T) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  z_t (*Ts)[kBT + 1] = reinterpret_cast<z_t (*)[kBT + 1]>(smraw);
-  z_t* col = reinterpret_cast<z_t*>(smraw) + kBT * (kBT + 1);
-  const int tid = threadIdx.x;
-  for (int e = tid; e < kBT * kBT; e += blockDim.x) Ts[e % kBT][e / kBT] = make_double2(0.0, 0.0);
-  __syncthreads();
-  for (int i = 0; i < kb; ++i) {
-    const z_t ti = tau[i];
-    if (tid < i) col[tid] = Gm[tid + int64_t(i) * kb];
-    __syncthreads();
-    if (tid < i) {
+// T factors of every block at once (zlarft forward/columnwise): one CTA per block, one
+// thread per row r of T: T(r,r) = tau_r, T(r,i) = -tau_i sum_{k=r}^{i-1} T(r,k) G(k,i).
+// A thread only reads its own row of T, so no barriers are needed.
+__global__ void __launch_bounds__(kBT) larft_all_kernel(const z_t* __restrict__ Gall,
+                                                         const z_t* __restrict__ tau,
+                                                         int64_t nref, z_t* __restrict__ Tall) {
+  const int b = blockIdx.x, r = threadIdx.x;
+  const z_t* G = Gall + int64_t(b) * kBT * kBT;
+  z_t* T = Tall + int64_t(b) * kBT * kBT;
+  const int64_t j0 = int64_t(b) * kBT;
+  auto tau_of = [&](int k) {
+    return (j0 + k < nref) ? tau[j0 + k] : make_double2(0.0, 0.0);
+  };
+  for (int i = 0; i < kBT; ++i) {
+    z_t v = make_double2(0.0, 0.0);
+    if (i == r) {
+      v = tau_of(r);
+    } else if (i > r) {
       z_t s = make_double2(0.0, 0.0);
-      for (int k = tid; k < i; ++k) zfma(s, Ts[tid][k], col[k]);
-      Ts[tid][i] = zscale(zmul(ti, s), -1.0);
+      for (int k = r; k < i; ++k) zfma(s, T[r + int64_t(k) * kBT], G[k + int64_t(i) * kBT]);
+      v = zscale(zmul(tau_of(i), s), -1.0);
     }
-    if (tid == 0) Ts[i][i] = ti;
-    __syncthreads();
+    T[r + int64_t(i) * kBT] = v;
   }
-  for (int e = tid; e < kb * kb; e += blockDim.x) T[(e % kb) + int64_t(e / kb) * kb] = Ts[e % kb][e / kb];
 }
 
 size_t unmtr_workspace_bytes(int64_t n, int64_t ncols) {
-  size_t z = size_t(n) * kBT            // Vb
-             + size_t(kBT) * kBT * 2    // G, T
-             + size_t(kBT) * ncols * 2  // W1, W2
-             + size_t(32) * kBT * ncols;  // split-K partials
-  return z * sizeof(z_t);
+  const int64_t nblk = ceil_div(max64(n, 1), kBT);
+  size_t z = 0;
+  z += size_t(n) * nblk * kBT * 2;       // Vall, VTall
+  z += size_t(nblk) * kBT * kBT * 2;     // Gall, Tall
+  z += size_t(kBT) * ncols;              // W1
+  z += size_t(16) * kBT * ncols;         // split-K partials
+  return z * sizeof(z_t) + 4096;
 }
 
-// Z <- H(0) H(1) ... H(nref-1) Z for the reflector family `mode` (see build_v_kernel).
+// Z <- H(0) H(1) ... H(nref-1) Z for the reflector family `mode`, applied in kBT-blocks from
+// the last to the first as Z <- Z - (V T)(V^H Z). V, T and V T of all blocks are formed up
+// front (batched), so the serial part per block is just two DMMA GEMMs.
 void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z_t* A,
                       int64_t lda, const z_t* tau, z_t* Z, int64_t ldz, int64_t ncols, void* ws) {
   if (nref <= 0 || ncols <= 0) return;
   const int off = mode == 1 ? 0 : 1;
-  z_t* Vb = reinterpret_cast<z_t*>(ws);
-  z_t* Gm = Vb + n * kBT;
-  z_t* T = Gm + kBT * kBT;
-  z_t* W1 = T + kBT * kBT;
-  z_t* W2 = W1 + int64_t(kBT) * ncols;
-  z_t* part = W2 + int64_t(kBT) * ncols;
-  const int64_t part_elems = int64_t(32) * kBT * ncols;
-  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
   const int64_t nblk = ceil_div(nref, kBT);
+  const int64_t ncol = nblk * kBT;
+  z_t* Vall = reinterpret_cast<z_t*>(ws);
+  z_t* VTall = Vall + n * ncol;
+  z_t* Gall = VTall + n * ncol;
+  z_t* Tall = Gall + nblk * kBT * kBT;
+  z_t* W1 = Tall + nblk * kBT * kBT;
+  z_t* part = W1 + int64_t(kBT) * ncols;
+  const int64_t part_elems = int64_t(16) * kBT * ncols;
+  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
+  {
+    const int blocks = int(min64(ceil_div(n * ncol, 256), 148 * 16));
+    build_vall_kernel<<<blocks, 256, 0, s>>>(A, lda, n, nref, ncol, mode, Vall);
+    BSE_LAUNCH_CHECK();
+  }
+  // G_b = V_b^H V_b (rows above a block are zero in Vall), all blocks in one launch
+  zgemm_batched(s, 1, 0, kBT, kBT, n, one, Vall, n, n * kBT, Vall, n, n * kBT, zero, Gall, kBT,
+                int64_t(kBT) * kBT, int(nblk));
+  larft_all_kernel<<<unsigned(nblk), kBT, 0, s>>>(Gall, tau, nref, Tall);
+  BSE_LAUNCH_CHECK();
+  // (V T)_b, all blocks in one launch
+  zgemm_batched(s, 0, 0, n, kBT, kBT, one, Vall, n, n * kBT, Tall, kBT, int64_t(kBT) * kBT, zero,
+                VTall, n, n * kBT, int(nblk));
   for (int64_t b = nblk - 1; b >= 0; --b) {
     const int64_t j0 = b * kBT;
-    const int kb = int(min64(kBT, nref - j0));
-    const int64_t m = n - j0 - off;
+    const int64_t r0 = j0 + off;  // first row any reflector of the block touches
+    const int64_t m = n - r0;
     if (m <= 0) continue;
-    {
-      const int blocks = int(min64(ceil_div(m * kb, 256), 148 * 8));
-      build_v_kernel<<<blocks, 256, 0, s>>>(A, lda, n, j0, kb, mode, Vb, m);
-      BSE_LAUNCH_CHECK();
-    }
-    // G = V^H V
-    zgemm(s, 1, 0, kb, kb, m, one, Vb, m, Vb, m, zero, Gm, kb, kGeneral, kGeneral, 0, part,
+    const z_t* Vb = Vall + j0 * n + r0;
+    const z_t* VTb = VTall + j0 * n + r0;
+    z_t* Zb = Z + r0;
+    // W1 = V_b^H Z (kBT x ncols, K = m; K-split on the under-filled grid)
+    zgemm(s, 1, 0, kBT, ncols, m, one, Vb, n, Zb, ldz, zero, W1, kBT, kGeneral, kGeneral, 0, part,
           part_elems);
-    {
-      const size_t sm = sizeof(z_t) * (kBT * (kBT + 1) + kBT);
-      static bool configured = false;
-      if (!configured) {
-        BSE_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(sm)));
-        configured = true;
-      }
-      larft_kernel<<<1, 64, sm, s>>>(Gm, kb, tau + j0, T);
-    }
-    BSE_LAUNCH_CHECK();
-    z_t* Zb = Z + (j0 + off);
-    // W1 = V^H Z  (kb x ncols)
-    zgemm(s, 1, 0, kb, ncols, m, one, Vb, m, Zb, ldz, zero, W1, kb, kGeneral, kGeneral, 0, part,
-          part_elems);
-    // W2 = T W1
-    zgemm(s, 0, 0, kb, ncols, kb, one, T, kb, W1, kb, zero, W2, kb, kUpperOp, kGeneral, 0,
-          nullptr, 0);
-    // Z -= V W2
-    zgemm(s, 0, 0, m, ncols, kb, mone, Vb, m, W2, kb, one, Zb, ldz, kGeneral, kGeneral, 0,
+    // Z -= (V T)_b W1
+    zgemm(s, 0, 0, m, ncols, kBT, mone, VTb, n, W1, kBT, one, Zb, ldz, kGeneral, kGeneral, 0,
           nullptr, 0);
   }
 }
