@@ -293,8 +293,11 @@ def main():
                     "per_launch_ms": gemm["ms"] / max(gemm["launches"], 1)}
     try:
         with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
-            tr = json.load(f)
-        roofline["traffic"] = tr.get(roofline["bound"])
+            tr = json.load(f).get(roofline["bound"], {})
+        if roofline["bound"] == "hbm" and "ratio" in tr:
+            # ncu dram bytes / algorithmic bytes of one captured launch, applied per launch
+            roofline["traffic"] = tr["ratio"] * roofline["algorithmic_bytes_per_launch"]
+            roofline["traffic_source"] = tr.get("capture")
     except Exception:
         pass
 
