@@ -243,8 +243,17 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
     if (last) break;
     grid.sync();
     // ---------------------------------------------------------------- P2: column reflector + y'
-    const double xn2 = gb_warp_sum_range(a.normp, s0, a.nch);
-    const z_t alpha = a.A[g + g * lda];
+    if (warp == 0) {  // one warp per CTA (no L2 hot spot), smem broadcast
+      const double v = gb_warp_sum_range(a.normp, s0, a.nch);
+      if (lane == 0) {
+        dred[0] = v;
+        xc[0] = a.A[g + g * lda];
+      }
+    }
+    __syncthreads();
+    const double xn2 = dred[0];
+    const z_t alpha = xc[0];
+    __syncthreads();
     double beta;
     z_t tq, scale;
     larfg_params2(alpha, xn2, beta, tq, scale);
@@ -389,8 +398,17 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
     // ---------------------------------------------------------------- P4: row reflector + x'
     if (has_cols) {
       const int c0 = int((g + 1) / kT);
-      const double xr2 = gb_warp_sum_range(a.normp, c0, a.nch);
-      const z_t alpha2 = a.wrow[g + 1];
+      if (warp == 0) {
+        const double v = gb_warp_sum_range(a.normp, c0, a.nch);
+        if (lane == 0) {
+          dred[0] = v;
+          xc[0] = a.wrow[g + 1];
+        }
+      }
+      __syncthreads();
+      const double xr2 = dred[0];
+      const z_t alpha2 = xc[0];
+      __syncthreads();
       double beta2;
       z_t tp, scale2;
       larfg_params2(alpha2, xr2, beta2, tp, scale2);

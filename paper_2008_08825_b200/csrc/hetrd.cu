@@ -21,6 +21,9 @@
 //    up front (batched); each 128-reflector block then costs two DMMA GEMMs.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+#include <vector>
+
 #include "blas.h"
 #include "gemm.cuh"
 #include "hetrd.h"
@@ -51,6 +54,7 @@ struct HetrdArgs {
   z_t* s12p;      // nch x 2NB: per-slab partial W^H x | V^H x
   z_t* t12;       // 2NB : t1 = W^H v | t2 = V^H v
   double* vav;    // gridDim.x : per-CTA partials of v^H A22 v
+  unsigned long long* trace;  // optional per-phase timestamps (BSE_HETRD_TRACE)
   int64_t p0;
   int nbp, nch;
 };
@@ -163,13 +167,31 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
   }
   grid.sync();
 
+  auto trace = [&](int i, int k) {
+    const int slab_owner = (a.nch - 1) % G;  // owner of the last slab (valid to the end)
+    if (a.trace && tid == 0 && (cta == 0 || cta == slab_owner)) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[((int64_t(a.p0 / NB) * NB + i) * 2 + (cta == 0 ? 0 : 1)) * 8 + k] = t;
+    }
+  };
   for (int i = 0; i < a.nbp; ++i) {
     const int64_t g = a.p0 + i;
     const int64_t g1 = g + 1;
     const bool has_next = (i + 1 < a.nbp);
+    trace(i, 0);
     // ---------------------------------------------------------------- phase A
-    const double xn2 = warp_sum_range(a.normp, int(g / kT), a.nch);
-    const z_t alpha = a.A[g1 + g * lda];  // g + 1 < n always (panels stop at n-2)
+    // one warp per CTA reduces the partial norms (avoids an L2 hot spot), smem broadcast
+    if (warp == 0) {
+      const double xn2w = warp_sum_range(a.normp, int(g / kT), a.nch);
+      if (lane == 0) {
+        dred[0] = xn2w;
+        zred[0] = a.A[g1 + g * lda];  // alpha; g + 1 < n always (panels stop at n-2)
+      }
+    }
+    __syncthreads();
+    const double xn2 = dred[0];
+    const z_t alpha = zred[0];
     double beta;
     z_t tau, scale;
     larfg_params(alpha, xn2, beta, tau, scale);
@@ -207,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
         }
       }
     }
+    trace(i, 1);
     // hemv over lower tiles of the trailing matrix rows/cols [g+1, n)
     {
       const int c0 = int(g1 / kT);
@@ -279,11 +302,17 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       const double vtot = block_sum(vav, dred);
       if (tid == 0) a.vav[cta] = vtot;
     }
+    trace(i, 2);
     grid.sync();
+    trace(i, 3);
     // ---------------------------------------------------------------- phase B
-    const double vav = warp_sum_range(a.vav, 0, G);
-    if (tid < 2 * NB) tt[tid] = a.t12[tid];  // zero beyond i
+    if (warp == 0) {
+      const double vw0 = warp_sum_range(a.vav, 0, G);
+      if (lane == 0) dred[1] = vw0;
+    }
+    if (tid >= 64 && tid < 64 + 2 * NB) tt[tid - 64] = a.t12[tid - 64];  // zero beyond i
     __syncthreads();
+    const double vav = dred[1];
     // v^H w' = v^H A v - sum_p [conj(t2_p) t1_p + conj(t1_p) t2_p]  (real)
     double vw = vav;
 #pragma unroll
@@ -401,7 +430,9 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       }
       __syncthreads();
     }
+    trace(i, 4);
     if (has_next) grid.sync();
+    trace(i, 5);
   }
 }
 
@@ -456,6 +487,9 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     return;
   }
   const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
+  const char* trace_path = getenv("BSE_HETRD_TRACE");
+  const size_t trace_n = size_t(ceil_div(n, NB)) * NB * 2 * 8;
+  if (trace_path) BSE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), trace_n * 8, s));
   for (int64_t p0 = 0; p0 < n - 1; p0 += NB) {
     const int nbp = int(min64(NB, n - 1 - p0));
     BSE_CUDA(cudaMemsetAsync(a.VW, 0, sizeof(z_t) * size_t(n) * 2 * NB * 2, s));
@@ -485,6 +519,20 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   }
   set_last_diag_kernel<<<1, 32, 0, s>>>(A, lda, n, d);
   BSE_LAUNCH_CHECK();
+  if (trace_path) {  // developer tracing: per-column phase timestamps of CTAs 0 and G-1
+    std::vector<unsigned long long> h(trace_n);
+    BSE_CUDA(cudaMemcpyAsync(h.data(), a.trace, trace_n * 8, cudaMemcpyDeviceToHost, s));
+    BSE_CUDA(cudaStreamSynchronize(s));
+    BSE_CUDA(cudaFree(a.trace));
+    if (FILE* f = fopen(trace_path, "w")) {
+      for (size_t r = 0; r < trace_n / 8; ++r) {
+        fprintf(f, "%zu,%zu", r / 2, r % 2);
+        for (int k = 0; k < 8; ++k) fprintf(f, ",%llu", h[r * 8 + k]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------
