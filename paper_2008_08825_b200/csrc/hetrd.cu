@@ -195,28 +195,9 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
     double beta;
     z_t tau, scale;
     larfg_params(alpha, xn2, beta, tau, scale);
-    if (cta == 0) {
-      if (tid == 0) {
-        a.e[g] = beta;
-        a.tau[g] = tau;
-      }
-      // t1 = W^H v, t2 = V^H v over rows >= g+1 (v(g+1) = 1, v(r) = scale x(r))
-      const int kk = tid >> 2, part = tid & 3;  // 64 sums x 4 partial lanes
-      const int p = kk & (NB - 1);
-      z_t s = zero;
-      if (p < i) s = zsum_strided(a.s12p + kk, 2 * NB, int(g / kT) + part, a.nch, 4);
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
-      if (part == 0 && kk < 2 * NB) {
-        z_t t = zero;
-        if (p < i) {
-          const z_t head = kk < NB ? W[g1 + int64_t(p) * ldp] : V[g1 + int64_t(p) * ldp];
-          t = zadd(zconj(head), zmul(scale, s));
-        }
-        a.t12[kk] = t;
-      }
+    if (cta == 0 && tid == 0) {
+      a.e[g] = beta;
+      a.tau[g] = tau;
     }
     // reflector vector into the panels (rows >= g+1 of the owned slabs)
     if (q == 0) {
@@ -301,6 +282,25 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       }
       const double vtot = block_sum(vav, dred);
       if (tid == 0) a.vav[cta] = vtot;
+    }
+    if (cta == G - 1) {  // the last CTA has the fewest tiles: t1/t2 off the critical path
+      // t1 = W^H v, t2 = V^H v over rows >= g+1 (v(g+1) = 1, v(r) = scale x(r))
+      const int kk = tid >> 2, part = tid & 3;  // 64 sums x 4 partial lanes
+      const int p = kk & (NB - 1);
+      z_t s = zero;
+      if (p < i) s = zsum_strided(a.s12p + kk, 2 * NB, int(g / kT) + part, a.nch, 4);
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
+      if (part == 0 && kk < 2 * NB) {
+        z_t t = zero;
+        if (p < i) {
+          const z_t head = kk < NB ? W[g1 + int64_t(p) * ldp] : V[g1 + int64_t(p) * ldp];
+          t = zadd(zconj(head), zmul(scale, s));
+        }
+        a.t12[kk] = t;
+      }
     }
     trace(i, 2);
     grid.sync();
