@@ -433,3 +433,56 @@ def test_cpp_dropin_binary(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+# ------------------------------------------------------------------ degenerate / clustered spectra
+@pytest.mark.parametrize("n", [3, 64, 100, 300])
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+def test_fully_degenerate_spectrum(n, method):
+    """kappa = 3 in the conditioned family: every eigenvalue equals sqrt(3)/2 (the D&C
+    deflates everything); any orthonormal basis is acceptable."""
+    a, b = configs.generate_conditioned(n, 3.0, 5)
+    r = bse.solve(method, bse.from_blocks(a, b))
+    assert np.allclose(r.lambda_, SQ3 / 2, rtol=1e-12)
+    assert residual(a, b, r.lambda_, r.v).max() <= 100 * n * EPS
+    assert sigma_orthogonality_error(r.v) <= 1e-10 * n
+
+
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+def test_identity_and_repeated_diagonal(method):
+    for a in (np.eye(150), np.diag(np.repeat([1.0, 2.0, 3.0], 70))):
+        n = a.shape[0]
+        r = bse.solve(method, bse.from_blocks(a, np.zeros((n, n))))
+        assert np.allclose(r.lambda_, np.sort(np.diag(a)), rtol=1e-13)
+        assert residual(a, np.zeros((n, n)), r.lambda_, r.v).max() <= 100 * n * EPS
+        assert sigma_orthogonality_error(r.v) <= 1e-10 * n
+
+
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+def test_clustered_spectrum(method):
+    """Tight clusters (gaps ~1e-9 relative) mixed with isolated eigenvalues."""
+    n = 240
+    q = configs.random_unitary(n, 17)
+    d = np.concatenate([1.0 + 1e-9 * np.arange(80), 2.0 + 1e-12 * np.arange(80),
+                        np.linspace(3.0, 9.0, 80)])
+    a = (q.conj().T * d[None, :]) @ q
+    a = 0.5 * (a + a.conj().T)
+    b = 0.25 * a
+    h = bse.from_blocks(a, b)
+    r = bse.solve(method, h)
+    lo, _, _ = oracle.solve(int(method), h.a, h.b)
+    assert np.max(np.abs(r.lambda_ - lo) / lo) <= 1e-10
+    assert residual(h.a, h.b, r.lambda_, r.v).max() <= 100 * n * EPS
+    assert sigma_orthogonality_error(r.v) <= 1e-10 * n
+
+
+@pytest.mark.parametrize("n", [2, 33, 200])
+def test_hermitian_eig_degenerate(n):
+    """Backend eig on a diagonal / identity / rank-1-perturbed identity."""
+    for m in (np.eye(n), np.diag(np.arange(n) % 3 + 1.0),
+              np.eye(n) + 1e-3 * np.outer(np.ones(n), np.ones(n))):
+        e = bse.hermitian_eig(m)
+        w = np.linalg.eigvalsh(m)
+        assert np.max(np.abs(e.values - w)) <= 100 * EPS * n * np.abs(w).max()
+        assert np.linalg.norm(m @ e.vectors - e.vectors * e.values[None, :]) <= 100 * EPS * n * max(np.linalg.norm(m), 1)
+        assert np.linalg.norm(e.vectors.conj().T @ e.vectors - np.eye(n)) <= 100 * EPS * n
