@@ -4,6 +4,10 @@
 // Replaces cblas_ztrsm (backend.cpp:124-127), cblas_ztrmm (backend.cpp:151-155, 161-165)
 // and cblas_zgemm (backend.cpp:170-173).
 #include "blas.h"
+
+#include <cudaTypedefs.h>
+
+#include "tile_ring.cuh"
 #include "gemm.cuh"
 
 namespace bseg {
@@ -311,6 +315,28 @@ void ztrsm_lower(cudaStream_t s, int side, int op, int64_t n, int64_t other, con
   ztrtri_diag_blocks(s, n, L, ldl, nb, inv);
   TrsmCtx c{s, L, ldl, inv, nb, side, op, tmp, part, 8 * n * int64_t(nb)};
   trsm_rec(c, 0, n, X, ldx, other);
+}
+
+CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    BSE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                     cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !encode)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {cuuint64_t(2 * n), cuuint64_t(n)};
+  const cuuint64_t strides[1] = {cuuint64_t(lda) * sizeof(z_t)};
+  const cuuint32_t box[2] = {16, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<z_t*>(A), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
+  return map;
 }
 
 }  // namespace bseg

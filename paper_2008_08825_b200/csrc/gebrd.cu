@@ -17,10 +17,14 @@
 // A -= [V X][Y U]^H is a single DMMA GEMM with k = 2 nb.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+#include <vector>
+
 #include "blas.h"
 #include "gemm.cuh"
 #include "hetrd.h"
 #include "svd.h"
+#include "tile_ring.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -32,9 +36,16 @@ constexpr int kThreads = 256;  // 4 threads per slab row/column
 constexpr int kQ = kThreads / kT;
 constexpr int kNB = kGebrdNB;
 static_assert(kNB % kQ == 0 && kNB <= 32, "panel width");
+// Tile ring: every CTA keeps its last kRing trailing-matrix tiles in shared memory. Within a
+// panel the trailing block A(p0:, p0:) is only read (zlabrd keeps the update in V,X,Y,U), so a
+// tile loaded once stays valid for all kNB columns; the two mat-vec sweeps per column run in
+// opposite directions (serpentine), each starting on the kRing tiles the previous sweep ended
+// on, and the refills stream kRing tiles ahead of the consumer.
+constexpr int kRing = 3;
+constexpr int kTile = kT * kT;  // z_t per slot (tile_ring.cuh layout)
 }  // namespace
 
-struct GebrdArgs {
+struct alignas(64) GebrdArgs {
   z_t* A;
   int64_t lda, n;
   double* d;
@@ -51,6 +62,8 @@ struct GebrdArgs {
   z_t* t;         // 4 (NB+1): t1 | t2 | t3 | t4
   int64_t p0;
   int nbp, nch;
+  unsigned long long* trace;  // optional per-phase timestamps (BSE_GEBRD_TRACE)
+  CUtensorMap tmap;           // TMA view of A (tile_ring.cuh)
 };
 
 __device__ __forceinline__ void larfg_params2(z_t alpha, double xnorm2, double& beta, z_t& tau,
@@ -81,17 +94,48 @@ __device__ __forceinline__ double gb_warp_sum_range(const double* p, int lo, int
   return warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
 }
 
+// sum_k p[k * es] over k = start, start + stride, ... < hi; loads issued 16 at a time (one
+// memory round trip for up to 16 terms), fixed summation order.
 __device__ __forceinline__ z_t gb_zsum_strided(const z_t* p, int64_t es, int start, int hi,
                                                int stride) {
-  z_t s[8];
+  z_t s[4];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) s[u] = make_double2(0.0, 0.0);
-  for (int k0 = start; k0 < hi; k0 += 8 * stride) {
+  for (int u = 0; u < 4; ++u) s[u] = make_double2(0.0, 0.0);
+  for (int k0 = start; k0 < hi; k0 += 16 * stride) {
+    z_t v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (k0 + u * stride < hi) s[u] = zadd(s[u], p[int64_t(k0 + u * stride) * es]);
+    for (int u = 0; u < 16; ++u)
+      v[u] = (k0 + u * stride < hi) ? p[int64_t(k0 + u * stride) * es] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s[u & 3] = zadd(s[u & 3], v[u]);
   }
-  return zadd(zadd(zadd(s[0], s[1]), zadd(s[2], s[3])), zadd(zadd(s[4], s[5]), zadd(s[6], s[7])));
+  return zadd(zadd(s[0], s[1]), zadd(s[2], s[3]));
+}
+
+// Sums each of 16 complex values over the 32 lanes of a warp by recursive halving (16
+// complex shuffles in all); on return lane l holds the total of value (l >> 1).
+__device__ __forceinline__ z_t gb_warp_transpose_sum16(z_t (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int st = 0; st < 4; ++st) {
+    const int h = 8 >> st, o = 16 >> st;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < h) {
+        const z_t keep = up ? v[h + j] : v[j];
+        const z_t send = up ? v[j] : v[h + j];
+        z_t r;
+        r.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+        r.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+        v[j] = zadd(keep, r);
+      }
+    }
+  }
+  z_t r;
+  r.x = __shfl_xor_sync(0xffffffffu, v[0].x, 1);
+  r.y = __shfl_xor_sync(0xffffffffu, v[0].y, 1);
+  return zadd(v[0], r);
 }
 
 __device__ __forceinline__ int gb_first_owned(int lo, int cta, int G) {
@@ -117,11 +161,84 @@ __device__ __forceinline__ void gb_tsum(const z_t* partial, int stride, int off,
                           : make_double2(0.0, 0.0);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
+// Tile k of this CTA in the panel's K x K tile grid starting at slab sp.
+__device__ __forceinline__ void gb_tile_coords(int k, int K, int sp, int& rc, int& cc) {
+  const int t = int(blockIdx.x) + k * int(gridDim.x);
+  rc = sp + t % K;
+  cc = sp + t / K;
+}
+
+using Ring = TileRing<kRing>;
+
+// One mat-vec sweep over this CTA's T tiles, writing one 64-vector partial per tile to P.
+//  kCols (P2): y(c) = sum_r conj(A(r,c)) v(r), v = [1; scale * A(g+1:, g)] on rows >= g
+//  !kCols (P4): x(r) = sum_c A(r,c) u(c),      u = [1; scale * w(g+2:)] on cols >= g+1
+// Masked rows/columns of the cached tiles hold finite panel-start data that either meets a
+// zero vector entry or produces a partial nobody reads (see the phase comments). Forward
+// sweeps end with tiles T-kRing..T-1 resident, backward sweeps with 0..kRing-1: each sweep
+// starts on the tiles the previous one ended on, and refills run kRing tiles ahead.
+template <bool kCols>
+__device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, z_t* vt, z_t* red, int T,
+                                         int K, int sp, bool forward, int64_t g, z_t scale) {
+  const int tid = threadIdx.x, rl = tid & (kT - 1), q = tid / kT;
+  const int64_t n = a.n;
+  const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
+  auto fetch = [&](int k) -> z_t {
+    int rc, cc;
+    gb_tile_coords(k, K, sp, rc, cc);
+    const int64_t e = int64_t(kCols ? rc : cc) * kT + tid;
+    if (kCols) return (e > g && e < n) ? a.A[e + g * a.lda] : zero;
+    return (e >= g + 2 && e < n) ? a.wrow[e] : zero;
+  };
+  z_t raw = zero;
+  if (tid < kT && T > 0) raw = fetch(forward ? 0 : T - 1);
+  for (int j = 0; j < T; ++j) {
+    const int k = forward ? j : T - 1 - j;
+    int rc, cc;
+    gb_tile_coords(k, K, sp, rc, cc);
+    if (tid < kT) {
+      const int64_t e = int64_t(kCols ? rc : cc) * kT + tid;
+      z_t v;
+      if (kCols) v = (e == g) ? one : ((e > g && e < n) ? zmul(scale, raw) : zero);
+      else v = (e == g + 1) ? one : ((e >= g + 2 && e < n) ? zmul(scale, raw) : zero);
+      vt[tid] = v;
+      if (j + 1 < T) raw = fetch(forward ? j + 1 : T - 2 - j);  // next tile's vector in flight
+    }
+    const int sl = k % kRing;
+    ring.acquire(sl);
+    __syncthreads();
+    const z_t* tl = ring.slot(sl);
+    z_t acc[4] = {zero, zero, zero, zero};  // four independent FMA chains
+    const int k0 = q * (kT / kQ);
+#pragma unroll
+    for (int kk = 0; kk < kT / kQ; ++kk) {
+      if (kCols) zcfma(acc[kk & 3], tl[ring_idx(k0 + kk, rl)], vt[k0 + kk]);
+      else zfma(acc[kk & 3], tl[ring_idx(rl, k0 + kk)], vt[k0 + kk]);
+    }
+    red[q * kT + rl] = zadd(zadd(acc[0], acc[1]), zadd(acc[2], acc[3]));
+    __syncthreads();
+    if (q == 0) {
+      z_t sum = red[rl];
+#pragma unroll
+      for (int qq = 1; qq < kQ; ++qq) sum = zadd(sum, red[qq * kT + rl]);
+      a.P[(int64_t(kCols ? cc : rc) * a.nch + (kCols ? rc : cc)) * kT + rl] = sum;
+    }
+    const int kn = forward ? k + kRing : k - kRing;  // the tile this slot serves next
+    if (kn >= 0 && kn < T) {
+      int rn, cn;
+      gb_tile_coords(kn, K, sp, rn, cn);
+      ring.issue(sl, &a.tmap, int64_t(rn) * kT, int64_t(cn) * kT);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_constant__ GebrdArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char sm[];
-  z_t* tile = reinterpret_cast<z_t*>(sm);  // kT x (kT+1)
-  z_t* vt = tile + kT * (kT + 1);          // kT vector over the reduced dimension
+  Ring ring;
+  unsigned char* const sm_ring = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);  // TMA swizzle
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_ring + sizeof(z_t) * kRing * kTile);
+  z_t* vt = reinterpret_cast<z_t*>(bars + 2 * kRing);  // kT vector over the reduced dimension
   z_t* red = vt + kT;                      // kQ x kT
   z_t* red2 = red + kQ * kT;               // kQ x kT
   z_t* sa = red2 + kQ * kT;                // NB+1
@@ -145,35 +262,70 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
   z_t* t4 = a.t + 3 * (kNB + 1);
   const z_t zero = make_double2(0.0, 0.0);
 
+  auto trace = [&](int i, int k) {
+    if (a.trace && tid == 0 && (cta == 0 || cta == (a.nch - 1) % G)) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[((int64_t(a.p0 / kNB) * kNB + i) * 2 + (cta == 0 ? 0 : 1)) * 8 + k] = t;
+    }
+  };
+  // panel tile grid: slabs [sp, nch)^2 (a panel never straddles a 64-slab)
+  const int sp = int(a.p0 / kT), K = a.nch - sp;
+  const int T = (K * K > cta) ? (K * K - cta + G - 1) / G : 0;
+  ring.init(reinterpret_cast<z_t*>(sm_ring), bars);
+  for (int k = 0; k < kRing && k < T; ++k) {  // in flight during the first P1
+    int rc, cc;
+    gb_tile_coords(k, K, sp, rc, cc);
+    ring.issue(k, &a.tmap, int64_t(rc) * kT, int64_t(cc) * kT);
+  }
   for (int i = 0; i <= a.nbp; ++i) {
     const int64_t g = a.p0 + i;
+    if (i < a.nbp) trace(i, 0);
     const bool last = (i == a.nbp);
     const int s0 = int(g / kT);
     // ---------------------------------------------------------------- P1 (rows)
     const bool have_prev = i > 0;  // previous column had a row reflector (g - 1 < n - 1)
     const z_t taup_prev = have_prev ? a.taup[g - 1] : zero;
-    if (!last && tid < kNB) {
-      sa[tid] = tid < i ? Y[g + int64_t(tid) * ldp] : zero;
-      sb[tid] = tid < i ? U[g + int64_t(tid) * ldp] : zero;
-    }
-    if (tid < 2 * (kNB + 1)) tt[tid] = have_prev ? a.t[2 * (kNB + 1) + tid] : zero;  // t3 | t4
-    __syncthreads();
-    for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
+    for (int c = gb_first_owned(s0, cta, G), first = 1; c < a.nch; c += G, first = 0) {
       const int64_t r = int64_t(c) * kT + rl;
       const bool valid = r < n && r >= g;
-      z_t xpart = zero, upd = zero, aold = zero;
+      // one memory round trip: partials, panel rows and (first slab) the small vectors
+      // (all loads are issued before the first consumer)
+      z_t xpart = zero, upd = zero, aold = zero, vr[kNB / kQ], xr[kNB / kQ];
+      z_t pa = zero, pb = zero, pt = zero;
+      if (first) {
+        if (!last && tid < i) {
+          pa = Y[g + int64_t(tid) * ldp];
+          pb = U[g + int64_t(tid) * ldp];
+        }
+        if (have_prev && tid < 2 * (kNB + 1)) pt = a.t[2 * (kNB + 1) + tid];  // t3 | t4
+      }
+#pragma unroll
+      for (int k = 0; k < kNB / kQ; ++k) {
+        const int p = q + k * kQ;
+        vr[k] = (valid && p < i) ? V[r + int64_t(p) * ldp] : zero;
+        xr[k] = (valid && p < i - 1) ? X[r + int64_t(p) * ldp] : zero;
+      }
+      if (valid && q == 0 && !last) aold = a.A[r + g * lda];
+      if (valid && have_prev)
+        xpart = gb_zsum_strided(a.P + int64_t(c) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
+      if (first) {
+        if (tid < kNB) {
+          sa[tid] = pa;
+          sb[tid] = pb;
+        }
+        if (tid < 2 * (kNB + 1)) tt[tid] = pt;
+        __syncthreads();
+      }
       if (valid) {
-        if (have_prev)
-          xpart = gb_zsum_strided(a.P + int64_t(c) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
-        if (q == 0 && !last) aold = a.A[r + g * lda];
 #pragma unroll
         for (int k = 0; k < kNB / kQ; ++k) {
           const int p = q + k * kQ;
           if (p < i) {
-            const z_t vrp = V[r + int64_t(p) * ldp];
+            const z_t vrp = vr[k];
             if (have_prev) xpart = zsub(xpart, zmul(vrp, tt[p]));
             if (p < i - 1) {
-              const z_t xrp = X[r + int64_t(p) * ldp];
+              const z_t xrp = xr[k];
               if (have_prev) xpart = zsub(xpart, zmul(xrp, tt[(kNB + 1) + p]));
               if (!last) upd = zadd(upd, zadd(zmul(vrp, zconj(sa[p])), zmul(xrp, zconj(sb[p]))));
             } else if (!last) {
@@ -215,33 +367,32 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
       }
       const double nrm = block_sum(q == 0 ? zabs2(x) : 0.0, dred);
       if (tid == 0) a.normp[c] = nrm;
+      {  // s12(p) = [V(:,p)^H x | X(:,p)^H x] over this slab, from the rows held in registers
+        const z_t xv = xs[rl], xp = xc[rl];
+        z_t pr[16];
 #pragma unroll
-      for (int k = 0; k < kNB / 8; ++k) {
-        const int p = warp + 8 * k;
-        if (p < i) {
-          z_t s1 = zero, s2 = zero;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = lane + 32 * h;
-            const int64_t rr = int64_t(c) * kT + j;
-            if (rr < n) {
-              const z_t xv = xs[j];
-              zcfma(s1, V[rr + int64_t(p) * ldp], xv);
-              zcfma(s2, (p == i - 1) ? xc[j] : X[rr + int64_t(p) * ldp], xv);
-            }
-          }
-          s1 = warp_zsum(s1);
-          s2 = warp_zsum(s2);
-          if (lane == 0) {
-            a.s12[int64_t(c) * 2 * kNB + p] = s1;
-            a.s12[int64_t(c) * 2 * kNB + kNB + p] = s2;
-          }
+        for (int k = 0; k < kNB / kQ; ++k) {
+          const int p = q + k * kQ;
+          pr[k] = zero;
+          pr[8 + k] = zero;
+          zcfma(pr[k], vr[k], xv);
+          zcfma(pr[8 + k], (p == i - 1) ? xp : xr[k], xv);
+        }
+        const z_t tot = gb_warp_transpose_sum16(pr);
+        const int idx = lane >> 1;
+        if ((warp & 1) && !(lane & 1)) red[q * 16 + idx] = tot;  // rows 32..63 of the slab
+        __syncthreads();
+        if (!(warp & 1) && !(lane & 1)) {
+          const int p = q + (idx & 7) * kQ;
+          if (p < i) a.s12[int64_t(c) * 2 * kNB + (idx >> 3) * kNB + p] = zadd(tot, red[q * 16 + idx]);
         }
       }
       __syncthreads();
     }
     if (last) break;
+    trace(i, 1);
     grid.sync();
+    trace(i, 2);
     // ---------------------------------------------------------------- P2: column reflector + y'
     if (warp == 0) {  // one warp per CTA (no L2 hot spot), smem broadcast
       const double v = gb_warp_sum_range(a.normp, s0, a.nch);
@@ -273,73 +424,48 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
       }
     }
     const bool has_cols = (g + 1 < n);
-    if (has_cols) {
-      const int r0c = s0, c0c = int((g + 1) / kT);
-      const int Kr = a.nch - r0c, Kc = a.nch - c0c;
-      const int64_t ntiles = int64_t(Kr) * Kc;
-      for (int64_t t = cta; t < ntiles; t += G) {
-        const int rc = r0c + int(t % Kr), cc = c0c + int(t / Kr);
-        const int64_t R0 = int64_t(rc) * kT, C0 = int64_t(cc) * kT;
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kT * kT / kThreads; ++k) {
-          const int e2 = tid + k * kThreads;
-          const int rr = e2 % kT, cl = e2 / kT;
-          const int64_t r = R0 + rr, c = C0 + cl;
-          const bool ok = r < n && c < n && r >= g && c > g;
-          cp_async16(tile + rr + cl * (kT + 1), ok ? a.A + r + c * lda : a.A, ok);
-        }
-        cp_async_commit();
-        if (tid < kT) {
-          const int64_t r = R0 + tid;
-          z_t v = zero;
-          if (r == g) v = make_double2(1.0, 0.0);
-          else if (r > g && r < n) v = zmul(scale, a.A[r + g * lda]);
-          vt[tid] = v;
-        }
-        cp_async_wait<0>();
-        __syncthreads();
-        z_t yc = zero;
-#pragma unroll 4
-        for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) zcfma(yc, tile[k + rl * (kT + 1)], vt[k]);
-        red[q * kT + rl] = yc;
-        __syncthreads();
-        if (q == 0) {
-          z_t s = red[rl];
-#pragma unroll
-          for (int qq = 1; qq < kQ; ++qq) s = zadd(s, red[qq * kT + rl]);
-          a.P[(int64_t(cc) * a.nch + rc) * kT + rl] = s;
-        }
-      }
-    }
+    if (has_cols) gb_sweep<true>(a, ring, vt, red, T, K, sp, true, g, scale);
+    trace(i, 3);
     grid.sync();
+    trace(i, 4);
     // ---------------------------------------------------------------- P3 (columns)
-    if (tid <= kNB) {
-      sa[tid] = (tid == i) ? make_double2(1.0, 0.0) : (tid < i ? V[g + int64_t(tid) * ldp] : zero);
-      sb[tid] = tid < i ? X[g + int64_t(tid) * ldp] : zero;
-    }
-    if (tid < 2 * (kNB + 1)) tt[tid] = a.t[tid];  // t1 | t2
-    __syncthreads();
-    if (q == 0) {  // reflector storage of column g (P2 readers are done)
-      for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
-        const int64_t r = int64_t(c) * kT + rl;
-        if (r < n && r > g) a.A[r + g * lda] = V[r + int64_t(i) * ldp];
-      }
-    }
     if (has_cols) {
       const int c0 = int((g + 1) / kT);
-      for (int cb = gb_first_owned(c0, cta, G); cb < a.nch; cb += G) {
+      for (int cb = gb_first_owned(c0, cta, G), first = 1; cb < a.nch; cb += G, first = 0) {
         const int64_t c = int64_t(cb) * kT + rl;
         const bool valid = c < n && c > g;
-        z_t ypart = zero, wpart = zero, aold = zero;
+        // one memory round trip: partials, panel rows and (first slab) the small vectors
+        z_t ypart = zero, wpart = zero, aold = zero, yr[kNB / kQ], ur[kNB / kQ];
+        z_t pa = zero, pb = zero, pt = zero;
+        if (first) {
+          if (tid < i) {
+            pa = V[g + int64_t(tid) * ldp];
+            pb = X[g + int64_t(tid) * ldp];
+          }
+          if (tid < 2 * (kNB + 1)) pt = a.t[tid];  // t1 | t2
+        }
+#pragma unroll
+        for (int k = 0; k < kNB / kQ; ++k) {
+          const int p = q + k * kQ;
+          yr[k] = (valid && p < i) ? Y[c + int64_t(p) * ldp] : zero;
+          ur[k] = (valid && p < i) ? U[c + int64_t(p) * ldp] : zero;
+        }
+        if (valid && q == 0) aold = a.A[g + c * lda];
+        if (valid) ypart = gb_zsum_strided(a.P + int64_t(cb) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
+        if (first) {
+          if (tid <= kNB) {
+            sa[tid] = (tid == i) ? make_double2(1.0, 0.0) : pa;
+            sb[tid] = pb;
+          }
+          if (tid < 2 * (kNB + 1)) tt[tid] = pt;
+          __syncthreads();
+        }
         if (valid) {
-          ypart = gb_zsum_strided(a.P + int64_t(cb) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
-          if (q == 0) aold = a.A[g + c * lda];
 #pragma unroll
           for (int k = 0; k < kNB / kQ; ++k) {
             const int p = q + k * kQ;
             if (p < i) {
-              const z_t ycp = Y[c + int64_t(p) * ldp], ucp = U[c + int64_t(p) * ldp];
+              const z_t ycp = yr[k], ucp = ur[k];
               ypart = zsub(ypart, zadd(zmul(ycp, tt[p]), zmul(ucp, tt[(kNB + 1) + p])));
               wpart = zadd(wpart, zadd(zmul(ycp, zconj(sa[p])), zmul(ucp, zconj(sb[p]))));
             }
@@ -368,33 +494,39 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
         }
         const double nrm = block_sum(q == 0 ? zabs2(w) : 0.0, dred);
         if (tid == 0) a.normp[cb] = nrm;
+        {  // s34(p) = [Y(:,p)^H w (p <= i) | U(:,p)^H w (p < i)] over this slab
+          const z_t wv = xs[rl], yc = xc[rl];
+          z_t pr[16];
 #pragma unroll
-        for (int k = 0; k < (kNB + 7) / 8 + 1; ++k) {
-          const int p = warp + 8 * k;
-          if (p <= i && p <= kNB) {
-            z_t s3 = zero, s4 = zero;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = lane + 32 * h;
-              const int64_t cc2 = int64_t(cb) * kT + j;
-              if (cc2 < n) {
-                const z_t wv = xs[j];
-                zcfma(s3, (p == i) ? xc[j] : Y[cc2 + int64_t(p) * ldp], wv);
-                if (p < i) zcfma(s4, U[cc2 + int64_t(p) * ldp], wv);
-              }
-            }
-            s3 = warp_zsum(s3);
-            s4 = warp_zsum(s4);
-            if (lane == 0) {
-              a.s34[int64_t(cb) * 2 * (kNB + 1) + p] = s3;
-              a.s34[int64_t(cb) * 2 * (kNB + 1) + (kNB + 1) + p] = s4;
-            }
+          for (int k = 0; k < kNB / kQ; ++k) {
+            const int p = q + k * kQ;
+            pr[k] = zero;
+            pr[8 + k] = zero;
+            zcfma(pr[k], (p == i) ? yc : yr[k], wv);
+            zcfma(pr[8 + k], ur[k], wv);
+          }
+          const z_t tot = gb_warp_transpose_sum16(pr);
+          const int idx = lane >> 1;
+          if ((warp & 1) && !(lane & 1)) red[q * 16 + idx] = tot;
+          __syncthreads();
+          if (!(warp & 1) && !(lane & 1)) {
+            const int p = q + (idx & 7) * kQ, kind = idx >> 3;
+            if (p < i || (p == i && kind == 0))
+              a.s34[int64_t(cb) * 2 * (kNB + 1) + kind * (kNB + 1) + p] = zadd(tot, red[q * 16 + idx]);
           }
         }
         __syncthreads();
       }
     }
+    if (q == 0) {  // reflector storage of column g (the P2 readers of A(:, g) are done)
+      for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
+        const int64_t r = int64_t(c) * kT + rl;
+        if (r < n && r > g) a.A[r + g * lda] = V[r + int64_t(i) * ldp];
+      }
+    }
+    trace(i, 5);
     grid.sync();
+    trace(i, 6);
     // ---------------------------------------------------------------- P4: row reflector + x'
     if (has_cols) {
       const int c0 = int((g + 1) / kT);
@@ -433,45 +565,12 @@ __global__ void __launch_bounds__(kThreads, 2) gebrd_panel_kernel(GebrdArgs a) {
           }
         }
       }
-      const int Kr = a.nch - c0, Kc = a.nch - c0;
-      const int64_t ntiles = int64_t(Kr) * Kc;
-      for (int64_t t = cta; t < ntiles; t += G) {
-        const int rc = c0 + int(t % Kr), cc = c0 + int(t / Kr);
-        const int64_t R0 = int64_t(rc) * kT, C0 = int64_t(cc) * kT;
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kT * kT / kThreads; ++k) {
-          const int e2 = tid + k * kThreads;
-          const int rr = e2 % kT, cl = e2 / kT;
-          const int64_t r = R0 + rr, c = C0 + cl;
-          const bool ok = r < n && c < n && r > g && c > g;
-          cp_async16(tile + rr + cl * (kT + 1), ok ? a.A + r + c * lda : a.A, ok);
-        }
-        cp_async_commit();
-        if (tid < kT) {
-          const int64_t c = C0 + tid;
-          z_t u = zero;
-          if (c == g + 1) u = make_double2(1.0, 0.0);
-          else if (c >= g + 2 && c < n) u = zmul(scale2, a.wrow[c]);
-          vt[tid] = u;
-        }
-        cp_async_wait<0>();
-        __syncthreads();
-        z_t xr = zero;
-#pragma unroll 4
-        for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) zfma(xr, tile[rl + k * (kT + 1)], vt[k]);
-        red[q * kT + rl] = xr;
-        __syncthreads();
-        if (q == 0) {
-          z_t s = red[rl];
-#pragma unroll
-          for (int qq = 1; qq < kQ; ++qq) s = zadd(s, red[qq * kT + rl]);
-          a.P[(int64_t(rc) * a.nch + cc) * kT + rl] = s;
-        }
-      }
+      gb_sweep<false>(a, ring, vt, red, T, K, sp, false, g, scale2);
     }
+    trace(i, 7);
     grid.sync();
   }
+  ring.drain();  // no bulk copy may be in flight when the CTA exits
 }
 
 size_t gebrd_workspace_bytes(int64_t n) {
@@ -493,6 +592,7 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   z_t* base = reinterpret_cast<z_t*>(ws);
   GebrdArgs a{};
   a.A = A; a.lda = lda; a.n = n; a.d = d; a.e = e; a.tauq = tauq; a.taup = taup;
+  a.tmap = make_tile_map(A, lda, n);
   a.VX = base; base += n * 2 * kNB;
   a.YU = base; base += n * 2 * kNB;
   a.wrow = base; base += n;
@@ -502,8 +602,8 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   a.t = base; base += 4 * (kNB + 1);
   a.normp = reinterpret_cast<double*>(base);
   a.nch = nch;
-  const size_t smem = (size_t(kT) * (kT + 1) + kT + 2 * kQ * kT + 4 * (kNB + 1) + 2 * kT) *
-                          sizeof(z_t) + 8 * sizeof(double);
+  const size_t smem = (size_t(kRing) * kTile + kRing + kT + 2 * kQ * kT + 4 * (kNB + 1) + 2 * kT) *
+                          sizeof(z_t) + 8 * sizeof(double) + 1024;
   static int blocks_per_sm = -1, num_sms = 0;
   if (blocks_per_sm < 0) {
     BSE_CUDA(cudaFuncSetAttribute(gebrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -516,6 +616,9 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     if (blocks_per_sm < 1) throw std::runtime_error("gebrd: kernel cannot be resident");
   }
   const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
+  const char* trace_path = getenv("BSE_GEBRD_TRACE");
+  const size_t trace_n = size_t(ceil_div(n, kNB)) * kNB * 2 * 8;
+  if (trace_path) BSE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), trace_n * 8, s));
   for (int64_t p0 = 0; p0 < n; p0 += kNB) {
     const int nbp = int(min64(kNB, n - p0));
     BSE_CUDA(cudaMemsetAsync(a.VX, 0, sizeof(z_t) * size_t(n) * 2 * kNB * 2, s));
@@ -541,6 +644,20 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
       // A(q:, q:) -= [V X](q:, :) [Y U](q:, :)^H
       zgemm(s, 0, 1, n - q, n - q, 2 * kNB, mone, a.VX + q, n, a.YU + q, n, one, A + q + q * lda,
             lda, kGeneral, kGeneral, 0, nullptr, 0);
+    }
+  }
+  if (trace_path) {  // developer tracing: per-column phase timestamps of two CTAs
+    std::vector<unsigned long long> h(trace_n);
+    BSE_CUDA(cudaMemcpyAsync(h.data(), a.trace, trace_n * 8, cudaMemcpyDeviceToHost, s));
+    BSE_CUDA(cudaStreamSynchronize(s));
+    BSE_CUDA(cudaFree(a.trace));
+    if (FILE* f = fopen(trace_path, "w")) {
+      for (size_t r = 0; r < trace_n / 8; ++r) {
+        fprintf(f, "%zu,%zu", r / 2, r % 2);
+        for (int k = 0; k < 8; ++k) fprintf(f, ",%llu", h[r * 8 + k]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
     }
   }
 }

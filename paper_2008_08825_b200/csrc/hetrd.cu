@@ -217,7 +217,10 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       const int K = a.nch - c0;
       const int64_t ntiles = int64_t(K) * (K + 1) / 2;
       double vav = 0.0;
-      for (int64_t t = cta; t < ntiles; t += G) {
+      for (int64_t tt = cta; tt < ntiles; tt += G) {
+        // alternate the sweep direction every column: the tiles streamed last by column g-1
+        // are still in L2 and are read first here (serpentine order)
+        const int64_t t = (g & 1) ? ntiles - 1 - tt : tt;
         int bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
         while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
         while (int64_t(bi) * (bi + 1) / 2 > t) --bi;
