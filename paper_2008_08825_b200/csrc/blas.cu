@@ -329,11 +329,11 @@ CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n) {
   CUtensorMap map;
   const cuuint64_t dims[2] = {cuuint64_t(2 * n), cuuint64_t(n)};
   const cuuint64_t strides[1] = {cuuint64_t(lda) * sizeof(z_t)};
-  const cuuint32_t box[2] = {16, 64};
+  const cuuint32_t box[2] = {128, 64};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<z_t*>(A), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
   return map;

@@ -147,6 +147,80 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// ------------------------------------------------------------------ latency-bound reductions
+// sum_k p[k * es] over k = start, start + stride, ... < hi; loads issued 16 at a time (one
+// memory round trip for up to 16 terms), fixed summation order.
+__device__ __forceinline__ z_t zsum_strided16(const z_t* p, int64_t es, int start, int hi,
+                                               int stride) {
+  z_t s[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) s[u] = make_double2(0.0, 0.0);
+  for (int k0 = start; k0 < hi; k0 += 16 * stride) {
+    z_t v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      v[u] = (k0 + u * stride < hi) ? p[int64_t(k0 + u * stride) * es] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s[u & 3] = zadd(s[u & 3], v[u]);
+  }
+  return zadd(zadd(s[0], s[1]), zadd(s[2], s[3]));
+}
+
+// Sums each of 16 complex values over the 32 lanes of a warp by recursive halving (16
+// complex shuffles in all); on return lane l holds the total of value (l >> 1).
+__device__ __forceinline__ z_t warp_transpose_zsum16(z_t (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int st = 0; st < 4; ++st) {
+    const int h = 8 >> st, o = 16 >> st;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < h) {
+        const z_t keep = up ? v[h + j] : v[j];
+        const z_t send = up ? v[j] : v[h + j];
+        z_t r;
+        r.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+        r.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+        v[j] = zadd(keep, r);
+      }
+    }
+  }
+  z_t r;
+  r.x = __shfl_xor_sync(0xffffffffu, v[0].x, 1);
+  r.y = __shfl_xor_sync(0xffffffffu, v[0].y, 1);
+  return zadd(v[0], r);
+}
+
+// Sums each of 8 complex values over the 32 lanes of a warp (9 complex shuffles in all); on
+// return lanes 4j..4j+3 hold the total of value j.
+__device__ __forceinline__ z_t warp_transpose_zsum8(z_t (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int st = 0; st < 3; ++st) {
+    const int h = 4 >> st, o = 16 >> st;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < h) {
+        const z_t keep = up ? v[h + j] : v[j];
+        const z_t send = up ? v[j] : v[h + j];
+        z_t r;
+        r.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+        r.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+        v[j] = zadd(keep, r);
+      }
+    }
+  }
+  z_t t = v[0];
+#pragma unroll
+  for (int o = 2; o >= 1; o >>= 1) {
+    t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+    t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+  }
+  return t;
+}
+
 // ------------------------------------------------------------------ FP64 tensor core (DMMA)
 // D(8x8) += A(8x4, row) * B(4x8, col); lane t holds A[t/4][t%4], B[t%4][t/4],
 // C[t/4][2(t%4)], C[t/4][2(t%4)+1]. Lowers to SASS DMMA.8x8x4.

@@ -42,6 +42,7 @@ static_assert(kNB % kQ == 0 && kNB <= 32, "panel width");
 // opposite directions (serpentine), each starting on the kRing tiles the previous sweep ended
 // on, and the refills stream kRing tiles ahead of the consumer.
 constexpr int kRing = 3;
+constexpr int kTabMax = 512;  // per-CTA tile list capacity (checked on the host)
 constexpr int kTile = kT * kT;  // z_t per slot (tile_ring.cuh layout)
 }  // namespace
 
@@ -94,50 +95,6 @@ __device__ __forceinline__ double gb_warp_sum_range(const double* p, int lo, int
   return warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
 }
 
-// sum_k p[k * es] over k = start, start + stride, ... < hi; loads issued 16 at a time (one
-// memory round trip for up to 16 terms), fixed summation order.
-__device__ __forceinline__ z_t gb_zsum_strided(const z_t* p, int64_t es, int start, int hi,
-                                               int stride) {
-  z_t s[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) s[u] = make_double2(0.0, 0.0);
-  for (int k0 = start; k0 < hi; k0 += 16 * stride) {
-    z_t v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      v[u] = (k0 + u * stride < hi) ? p[int64_t(k0 + u * stride) * es] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < 16; ++u) s[u & 3] = zadd(s[u & 3], v[u]);
-  }
-  return zadd(zadd(s[0], s[1]), zadd(s[2], s[3]));
-}
-
-// Sums each of 16 complex values over the 32 lanes of a warp by recursive halving (16
-// complex shuffles in all); on return lane l holds the total of value (l >> 1).
-__device__ __forceinline__ z_t gb_warp_transpose_sum16(z_t (&v)[16]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int st = 0; st < 4; ++st) {
-    const int h = 8 >> st, o = 16 >> st;
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j < h) {
-        const z_t keep = up ? v[h + j] : v[j];
-        const z_t send = up ? v[j] : v[h + j];
-        z_t r;
-        r.x = __shfl_xor_sync(0xffffffffu, send.x, o);
-        r.y = __shfl_xor_sync(0xffffffffu, send.y, o);
-        v[j] = zadd(keep, r);
-      }
-    }
-  }
-  z_t r;
-  r.x = __shfl_xor_sync(0xffffffffu, v[0].x, 1);
-  r.y = __shfl_xor_sync(0xffffffffu, v[0].y, 1);
-  return zadd(v[0], r);
-}
-
 __device__ __forceinline__ int gb_first_owned(int lo, int cta, int G) {
   int c = cta;
   while (c < lo) c += G;
@@ -151,7 +108,7 @@ __device__ __forceinline__ void gb_tsum(const z_t* partial, int stride, int off,
                                         z_t scale, z_t* t_out, int nsum) {
   const int kk = threadIdx.x >> 2, part = threadIdx.x & 3;
   z_t s = make_double2(0.0, 0.0);
-  if (kk < nsum && kk < pmax) s = gb_zsum_strided(partial + off + kk, stride, c_lo + part, c_hi, 4);
+  if (kk < nsum && kk < pmax) s = zsum_strided16(partial + off + kk, stride, c_lo + part, c_hi, 4);
   s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
   s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
   s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
@@ -176,58 +133,81 @@ using Ring = TileRing<kRing>;
 // Masked rows/columns of the cached tiles hold finite panel-start data that either meets a
 // zero vector entry or produces a partial nobody reads (see the phase comments). Forward
 // sweeps end with tiles T-kRing..T-1 resident, backward sweeps with 0..kRing-1: each sweep
-// starts on the tiles the previous one ended on, and refills run kRing tiles ahead.
+// starts on the tiles the previous one ended on, and refills run kRing-1 tiles ahead.
+// Mapping: warp w owns tile columns 8w..8w+7, lane l rows l and l+32; column sums reduce
+// inside the warp (transpose reduction), row sums across warps through rowred (double
+// buffered, summed by warps 0-1 after the per-tile barrier). One CTA barrier per tile.
 template <bool kCols>
-__device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, z_t* vt, z_t* red, int T,
-                                         int K, int sp, bool forward, int64_t g, z_t scale) {
-  const int tid = threadIdx.x, rl = tid & (kT - 1), q = tid / kT;
+__device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const int* ttab,
+                                         z_t* vbuf, z_t* swp, int T, bool forward, int64_t g,
+                                         z_t scale) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
   const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
+  auto vidx = [&](int k) -> int64_t {
+    const int t = ttab[k];
+    return int64_t(kCols ? (t & 0xffff) : (t >> 16)) * kT + tid;
+  };
   auto fetch = [&](int k) -> z_t {
-    int rc, cc;
-    gb_tile_coords(k, K, sp, rc, cc);
-    const int64_t e = int64_t(kCols ? rc : cc) * kT + tid;
+    const int64_t e = vidx(k);
     if (kCols) return (e > g && e < n) ? a.A[e + g * a.lda] : zero;
     return (e >= g + 2 && e < n) ? a.wrow[e] : zero;
   };
+  auto put = [&](int k, z_t rw, z_t* buf) {
+    const int64_t e = vidx(k);
+    if (kCols) buf[tid] = (e == g) ? one : ((e > g && e < n) ? zmul(scale, rw) : zero);
+    else buf[tid] = (e == g + 1) ? one : ((e >= g + 2 && e < n) ? zmul(scale, rw) : zero);
+  };
   z_t raw = zero;
-  if (tid < kT && T > 0) raw = fetch(forward ? 0 : T - 1);
+  if (tid < kT && T > 0) {
+    put(forward ? 0 : T - 1, fetch(forward ? 0 : T - 1), vbuf);
+    if (T > 1) raw = fetch(forward ? 1 : T - 2);
+  }
+  __syncthreads();
   for (int j = 0; j < T; ++j) {
     const int k = forward ? j : T - 1 - j;
-    int rc, cc;
-    gb_tile_coords(k, K, sp, rc, cc);
-    if (tid < kT) {
-      const int64_t e = int64_t(kCols ? rc : cc) * kT + tid;
-      z_t v;
-      if (kCols) v = (e == g) ? one : ((e > g && e < n) ? zmul(scale, raw) : zero);
-      else v = (e == g + 1) ? one : ((e >= g + 2 && e < n) ? zmul(scale, raw) : zero);
-      vt[tid] = v;
-      if (j + 1 < T) raw = fetch(forward ? j + 1 : T - 2 - j);  // next tile's vector in flight
+    const int rc = ttab[k] & 0xffff, cc = ttab[k] >> 16;
+    ring.acquire(k % kRing);
+    const z_t* vv = vbuf + (j & 1) * kT;
+    if (tid < kT && j + 1 < T) {  // next tile's vector into the other buffer
+      put(forward ? j + 1 : T - 2 - j, raw, vbuf + ((j + 1) & 1) * kT);
+      if (j + 2 < T) raw = fetch(forward ? j + 2 : T - 3 - j);
     }
-    const int sl = k % kRing;
-    ring.acquire(sl);
-    __syncthreads();
-    const z_t* tl = ring.slot(sl);
-    z_t acc[4] = {zero, zero, zero, zero};  // four independent FMA chains
-    const int k0 = q * (kT / kQ);
+    const z_t* tl = ring.slot(k % kRing);
+    z_t* rowred = swp + (j & 1) * 8 * kT;
+    if (kCols) {
+      const z_t v0 = vv[lane], v1 = vv[lane + 32];
+      z_t pc[8];
 #pragma unroll
-    for (int kk = 0; kk < kT / kQ; ++kk) {
-      if (kCols) zcfma(acc[kk & 3], tl[ring_idx(k0 + kk, rl)], vt[k0 + kk]);
-      else zfma(acc[kk & 3], tl[ring_idx(rl, k0 + kk)], vt[k0 + kk]);
-    }
-    red[q * kT + rl] = zadd(zadd(acc[0], acc[1]), zadd(acc[2], acc[3]));
-    __syncthreads();
-    if (q == 0) {
-      z_t sum = red[rl];
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const int c = 8 * warp + c8;
+        pc[c8] = zero;
+        zcfma(pc[c8], tl[ring_idx(lane, c)], v0);
+        zcfma(pc[c8], tl[ring_idx(lane + 32, c)], v1);
+      }
+      const z_t tot = warp_transpose_zsum8(pc);
+      if ((lane & 3) == 0) a.P[(int64_t(cc) * a.nch + rc) * kT + 8 * warp + (lane >> 2)] = tot;
+    } else {
+      z_t r0 = zero, r1 = zero;
 #pragma unroll
-      for (int qq = 1; qq < kQ; ++qq) sum = zadd(sum, red[qq * kT + rl]);
-      a.P[(int64_t(kCols ? cc : rc) * a.nch + (kCols ? rc : cc)) * kT + rl] = sum;
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const int c = 8 * warp + c8;
+        const z_t u = vv[c];
+        zfma(r0, tl[ring_idx(lane, c)], u);
+        zfma(r1, tl[ring_idx(lane + 32, c)], u);
+      }
+      rowred[warp * kT + lane] = r0;
+      rowred[warp * kT + lane + 32] = r1;
     }
-    const int kn = forward ? k + kRing : k - kRing;  // the tile this slot serves next
-    if (kn >= 0 && kn < T) {
-      int rn, cn;
-      gb_tile_coords(kn, K, sp, rn, cn);
-      ring.issue(sl, &a.tmap, int64_t(rn) * kT, int64_t(cn) * kT);
+    __syncthreads();  // tile k fully read; partials and the next vector visible
+    const int kn = forward ? k + kRing : k - kRing;  // refill the slot with the tile it serves next
+    if (kn >= 0 && kn < T)
+      ring.issue(k % kRing, &a.tmap, int64_t(ttab[kn] & 0xffff) * kT, int64_t(ttab[kn] >> 16) * kT);
+    if (!kCols && tid < kT) {
+      z_t sum = rowred[tid];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) sum = zadd(sum, rowred[w * kT + tid]);
+      a.P[(int64_t(rc) * a.nch + cc) * kT + tid] = sum;
     }
   }
 }
@@ -236,12 +216,14 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char sm[];
   Ring ring;
-  unsigned char* const sm_ring = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);  // TMA swizzle
+  unsigned char* const sm_ring = sm + ((128u - (smem_u32(sm) & 127u)) & 127u);  // TMA alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_ring + sizeof(z_t) * kRing * kTile);
-  z_t* vt = reinterpret_cast<z_t*>(bars + 2 * kRing);  // kT vector over the reduced dimension
-  z_t* red = vt + kT;                      // kQ x kT
+  z_t* vbuf = reinterpret_cast<z_t*>(bars + 2 * kRing);  // 2 x kT: sweep vectors
+  int* ttab = reinterpret_cast<int*>(vbuf + 2 * kT);       // this CTA's tiles: rc | cc << 16
+  z_t* swp = reinterpret_cast<z_t*>(ttab + kTabMax);       // 2 x 8 x kT: sweep row partials
+  z_t* red = swp;                          // kQ x kT (P1/P3; aliases swp)
   z_t* red2 = red + kQ * kT;               // kQ x kT
-  z_t* sa = red2 + kQ * kT;                // NB+1
+  z_t* sa = swp + 2 * 8 * kT;              // NB+1
   z_t* sb = sa + (kNB + 1);                // NB+1
   z_t* tt = sb + (kNB + 1);                // 2(NB+1)
   z_t* xs = tt + 2 * (kNB + 1);            // kT
@@ -272,12 +254,14 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
   // panel tile grid: slabs [sp, nch)^2 (a panel never straddles a 64-slab)
   const int sp = int(a.p0 / kT), K = a.nch - sp;
   const int T = (K * K > cta) ? (K * K - cta + G - 1) / G : 0;
-  ring.init(reinterpret_cast<z_t*>(sm_ring), bars);
-  for (int k = 0; k < kRing && k < T; ++k) {  // in flight during the first P1
+  for (int k = tid; k < T; k += kThreads) {
     int rc, cc;
     gb_tile_coords(k, K, sp, rc, cc);
-    ring.issue(k, &a.tmap, int64_t(rc) * kT, int64_t(cc) * kT);
+    ttab[k] = rc | (cc << 16);
   }
+  ring.init(reinterpret_cast<z_t*>(sm_ring), bars);
+  for (int k = 0; k < kRing && k < T; ++k)  // in flight during the first P1 (ttab synced by init)
+    ring.issue(k, &a.tmap, int64_t(ttab[k] & 0xffff) * kT, int64_t(ttab[k] >> 16) * kT);
   for (int i = 0; i <= a.nbp; ++i) {
     const int64_t g = a.p0 + i;
     if (i < a.nbp) trace(i, 0);
@@ -308,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
       }
       if (valid && q == 0 && !last) aold = a.A[r + g * lda];
       if (valid && have_prev)
-        xpart = gb_zsum_strided(a.P + int64_t(c) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
+        xpart = zsum_strided16(a.P + int64_t(c) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
       if (first) {
         if (tid < kNB) {
           sa[tid] = pa;
@@ -378,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
           zcfma(pr[k], vr[k], xv);
           zcfma(pr[8 + k], (p == i - 1) ? xp : xr[k], xv);
         }
-        const z_t tot = gb_warp_transpose_sum16(pr);
+        const z_t tot = warp_transpose_zsum16(pr);
         const int idx = lane >> 1;
         if ((warp & 1) && !(lane & 1)) red[q * 16 + idx] = tot;  // rows 32..63 of the slab
         __syncthreads();
@@ -424,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
       }
     }
     const bool has_cols = (g + 1 < n);
-    if (has_cols) gb_sweep<true>(a, ring, vt, red, T, K, sp, true, g, scale);
+    if (has_cols) gb_sweep<true>(a, ring, ttab, vbuf, swp, T, true, g, scale);
     trace(i, 3);
     grid.sync();
     trace(i, 4);
@@ -451,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
           ur[k] = (valid && p < i) ? U[c + int64_t(p) * ldp] : zero;
         }
         if (valid && q == 0) aold = a.A[g + c * lda];
-        if (valid) ypart = gb_zsum_strided(a.P + int64_t(cb) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
+        if (valid) ypart = zsum_strided16(a.P + int64_t(cb) * a.nch * kT + rl, kT, s0 + q, a.nch, kQ);
         if (first) {
           if (tid <= kNB) {
             sa[tid] = (tid == i) ? make_double2(1.0, 0.0) : pa;
@@ -505,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
             zcfma(pr[k], (p == i) ? yc : yr[k], wv);
             zcfma(pr[8 + k], ur[k], wv);
           }
-          const z_t tot = gb_warp_transpose_sum16(pr);
+          const z_t tot = warp_transpose_zsum16(pr);
           const int idx = lane >> 1;
           if ((warp & 1) && !(lane & 1)) red[q * 16 + idx] = tot;
           __syncthreads();
@@ -565,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
           }
         }
       }
-      gb_sweep<false>(a, ring, vt, red, T, K, sp, false, g, scale2);
+      gb_sweep<false>(a, ring, ttab, vbuf, swp, T, false, g, scale2);
     }
     trace(i, 7);
     grid.sync();
@@ -602,8 +586,8 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   a.t = base; base += 4 * (kNB + 1);
   a.normp = reinterpret_cast<double*>(base);
   a.nch = nch;
-  const size_t smem = (size_t(kRing) * kTile + kRing + kT + 2 * kQ * kT + 4 * (kNB + 1) + 2 * kT) *
-                          sizeof(z_t) + 8 * sizeof(double) + 1024;
+  const size_t smem = (size_t(kRing) * kTile + kRing + 2 * kT + 2 * 8 * kT + 4 * (kNB + 1) + 2 * kT) *
+                          sizeof(z_t) + kTabMax * sizeof(int) + 8 * sizeof(double) + 128;
   static int blocks_per_sm = -1, num_sms = 0;
   if (blocks_per_sm < 0) {
     BSE_CUDA(cudaFuncSetAttribute(gebrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,6 +612,11 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     const int64_t tiles = ceil_div(m, kT) * ceil_div(m, kT);
     int G = int(min64(int64_t(blocks_per_sm) * num_sms, tiles));
     G = max(G, 1);
+    {
+      const int64_t K = nch - p0 / kT;
+      if (ceil_div(K * K, int64_t(G)) > kTabMax)
+        throw std::runtime_error("gebrd: matrix too large for the per-CTA tile list");
+    }
     void* args[] = {&a};
     double bytes = 0.0;  // algorithmic: A^H v over (n-g) x (n-g-1) and A u over (n-g-1)^2
     for (int i = 0; i < nbp; ++i) {

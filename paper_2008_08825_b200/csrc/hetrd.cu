@@ -27,6 +27,7 @@
 #include "blas.h"
 #include "gemm.cuh"
 #include "hetrd.h"
+#include "tile_ring.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -40,7 +41,7 @@ constexpr int kQ = kThreads / kT;
 static_assert(NB % kQ == 0 && NB <= 32, "panel width");
 }  // namespace
 
-struct HetrdArgs {
+struct alignas(64) HetrdArgs {
   z_t* A;
   int64_t lda, n;
   double* d;
@@ -55,6 +56,7 @@ struct HetrdArgs {
   z_t* t12;       // 2NB : t1 = W^H v | t2 = V^H v
   double* vav;    // gridDim.x : per-CTA partials of v^H A22 v
   unsigned long long* trace;  // optional per-phase timestamps (BSE_HETRD_TRACE)
+  CUtensorMap tmap;           // TMA view of A (tile_ring.cuh)
   int64_t p0;
   int nbp, nch;
 };
@@ -93,20 +95,6 @@ __device__ __forceinline__ double warp_sum_range(const double* p, int lo, int hi
   return warp_sum(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
 }
 
-// sum_{k = start, start + stride, ... < hi} p[k * es] (complex), 8 loads in flight.
-__device__ __forceinline__ z_t zsum_strided(const z_t* p, int64_t es, int start, int hi,
-                                            int stride) {
-  z_t s[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) s[u] = make_double2(0.0, 0.0);
-  for (int k0 = start; k0 < hi; k0 += 8 * stride) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (k0 + u * stride < hi) s[u] = zadd(s[u], p[int64_t(k0 + u * stride) * es]);
-  }
-  return zadd(zadd(zadd(s[0], s[1]), zadd(s[2], s[3])), zadd(zadd(s[4], s[5]), zadd(s[6], s[7])));
-}
-
 // First slab >= lo owned by this CTA (slab c belongs to CTA c % G); no integer division.
 __device__ __forceinline__ int first_owned(int lo, int cta, int G) {
   int c = cta;
@@ -114,23 +102,45 @@ __device__ __forceinline__ int first_owned(int lo, int cta, int G) {
   return c;
 }
 
+constexpr int kRing = 3;
+constexpr int kTabMax = 512;  // per-CTA tile list capacity (host caps the grid accordingly)
+using Ring = TileRing<kRing>;
+
+// Lower tile t (row-major over the triangle: (0,0), (1,0), (1,1), (2,0), ...) -> (bi, bj).
+__device__ __forceinline__ void tri_coords(int64_t t, int& bi, int& bj) {
+  bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+  while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
+  while (int64_t(bi) * (bi + 1) / 2 > t) --bi;
+  bj = int(t - int64_t(bi) * (bi + 1) / 2);
+}
+
 // One cooperative launch per nb-column panel. Per column g (index i in the panel):
-//   phase A : reflector from the partial norms (zlarfg, redundantly per CTA), v into the
-//             panel, Hermitian mat-vec y = A22 v over 64x64 lower tiles (each tile adds
-//             A_t v to its row chunk and A_t^H v to its column chunk) + per-CTA v^H A22 v;
+//   phase A : reflector from the partial norms (zlarfg, redundantly per CTA) and the
+//             Hermitian mat-vec y = A22 v over this CTA's 64x64 lower tiles (each tile adds
+//             A_t v to its row chunk and A_t^H v to its column chunk) + per-CTA v^H A22 v.
+//             The tiles stream through a TMA ring (tile_ring.cuh): A22 is read-only inside a
+//             panel, so consecutive columns sweep the CTA's tile list in alternating directions
+//             and start on the kRing tiles the previous sweep left in shared memory;
 //   phase B : alpha = -1/2 |tau|^2 (v^H A v - 2 Re t1^H t2) (no separate dot reduction),
 //             W(:,i) = tau (y - V t1 - W t2) + alpha v, and the NEXT column's update
 //             a(:,g+1) -= V W(g+1,:)^H + W V(g+1,:)^H with its partial norms / W^H x / V^H x.
+//             All of the phase's loads are issued before the first consumer (one round trip).
 // => two grid barriers per column; every partial sum has a fixed order (deterministic).
-__global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
+// Tile entries outside the live region (rows/cols < g+1, finite panel-start data) meet zero
+// vector entries or feed partials that are never read; the strict upper triangle of a
+// diagonal tile (never written, may hold garbage) is excluded by selects.
+__global__ void __launch_bounds__(kThreads, 1)
+    hetrd_panel_kernel(const __grid_constant__ HetrdArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char sm[];
-  z_t* tile = reinterpret_cast<z_t*>(sm);  // kT x (kT+1) column-major
-  z_t* vr = tile + kT * (kT + 1);          // v over tile rows
-  z_t* vc = vr + kT;                       // v over tile cols
-  z_t* red = vc + kT;                      // kQ x kT reduction scratch
+  unsigned char* const sm_ring = sm + ((128u - (smem_u32(sm) & 127u)) & 127u);  // TMA alignment
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_ring + sizeof(z_t) * kRing * kRingT * kRingT);
+  z_t* vbuf = reinterpret_cast<z_t*>(bars + 2 * kRing);  // 2 x [v rows | v cols] of a tile
+  int* ttab = reinterpret_cast<int*>(vbuf + 4 * kT);       // this CTA's tiles: bi | bj << 16
+  z_t* swp = reinterpret_cast<z_t*>(ttab + kTabMax);       // 2 x (8 x kT + kT): sweep partials
+  z_t* red = swp;                          // kQ x kT reduction scratch (phase B; aliases swp)
   z_t* red2 = red + kQ * kT;               // kQ x kT reduction scratch
-  z_t* wg = red2 + kQ * kT;                // NB : W(g+1, p)
+  z_t* wg = swp + 2 * (8 * kT + kT);       // NB : W(g+1, p)
   z_t* vg = wg + NB;                       // NB : V(g+1, p)
   z_t* xs = vg + NB;                       // kT : next column values of the slab
   z_t* wc = xs + kT;                       // kT : W(r, i) of the slab
@@ -144,7 +154,21 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
   const int64_t n = a.n, lda = a.lda, ldp = a.ldp;
   z_t* V = a.VW;
   z_t* W = a.VW + int64_t(NB) * ldp;
-  const z_t zero = make_double2(0.0, 0.0);
+  const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
+
+  // panel tile list: lower tiles of slabs [sp, nch) (a panel never straddles a 64-slab)
+  const int sp = int((a.p0 + 1) / kT), K = a.nch - sp;
+  const int ntiles = K * (K + 1) / 2;
+  const int T = ntiles > cta ? (ntiles - cta + G - 1) / G : 0;
+  for (int k = tid; k < T; k += kThreads) {
+    int bi, bj;
+    tri_coords(cta + int64_t(k) * G, bi, bj);
+    ttab[k] = bi | (bj << 16);
+  }
+  Ring ring;
+  ring.init(reinterpret_cast<z_t*>(sm_ring), bars);
+  for (int k = 0; k < kRing && k < T; ++k)  // in flight during phase 0 (ttab visible: init synced)
+    ring.issue(k, &a.tmap, int64_t(sp + (ttab[k] & 0xffff)) * kT, int64_t(sp + (ttab[k] >> 16)) * kT);
 
   // ---------------------------------------------------------------- phase 0: column p0
   {
@@ -181,6 +205,15 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
     const bool has_next = (i + 1 < a.nbp);
     trace(i, 0);
     // ---------------------------------------------------------------- phase A
+    const bool fwd = (i & 1) == 0;
+    // raw A(:, g) entries of a tile's row (tid < 64) / column (64 <= tid < 128) chunk
+    auto fetch = [&](int k) -> z_t {
+      const int bi = ttab[k] & 0xffff, bj = ttab[k] >> 16;
+      const int64_t e = int64_t(sp + (tid < kT ? bi : bj)) * kT + (tid & (kT - 1));
+      return (e > g1 && e < n) ? a.A[e + g * lda] : zero;
+    };
+    z_t raw = zero;
+    if (tid < 2 * kT && T > 0) raw = fetch(fwd ? 0 : T - 1);
     // one warp per CTA reduces the partial norms (avoids an L2 hot spot), smem broadcast
     if (warp == 0) {
       const double xn2w = warp_sum_range(a.normp, int(g / kT), a.nch);
@@ -199,99 +232,108 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       a.e[g] = beta;
       a.tau[g] = tau;
     }
+    trace(i, 1);
+    // v restricted to tile k's row chunk (tid < 64) / column chunk (64 <= tid < 128)
+    auto put_v = [&](int k, z_t rw, z_t* buf) {
+      const int bi = ttab[k] & 0xffff, bj = ttab[k] >> 16;
+      const int64_t e = int64_t(sp + (tid < kT ? bi : bj)) * kT + (tid & (kT - 1));
+      buf[tid] = (e == g1) ? one : ((e > g1 && e < n) ? zmul(scale, rw) : zero);
+    };
+    if (tid < 2 * kT && T > 0) {
+      put_v(fwd ? 0 : T - 1, raw, vbuf);
+      raw = (T > 1) ? fetch(fwd ? 1 : T - 2) : zero;
+    }
+    __syncthreads();
+    // Sweep: warp w owns tile columns 8w..8w+7, lane l rows l and l+32. Each element is read
+    // once for both products: row outputs reduce across warps (rowred, summed by warps 0-1
+    // after the barrier), column outputs within the warp (transpose reduction).
+    double vav = 0.0;
+    for (int j = 0; j < T; ++j) {
+      const int k = fwd ? j : T - 1 - j;
+      const int bi = ttab[k] & 0xffff, bj = ttab[k] >> 16;
+      const bool diag = (bi == bj);
+      ring.acquire(k % kRing);
+      const z_t* vr = vbuf + (j & 1) * 2 * kT;  // v over tile rows
+      const z_t* vc = vr + kT;                  // v over tile cols
+      z_t vrv = zero, vcv = zero;               // this row's entries, for v^H A v below
+      if (tid < kT) {
+        vrv = vr[tid];
+        vcv = vc[tid];
+      }
+      if (tid < 2 * kT && j + 1 < T) {  // next tile's vectors into the other buffer
+        put_v(fwd ? j + 1 : T - 2 - j, raw, vbuf + ((j + 1) & 1) * 2 * kT);
+        if (j + 2 < T) raw = fetch(fwd ? j + 2 : T - 3 - j);
+      }
+      const z_t* tl = ring.slot(k % kRing);
+      const z_t v0 = vr[lane], v1 = vr[lane + 32];
+      z_t r0 = zero, r1 = zero, pc[8];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const int c = 8 * warp + cc;
+        const z_t a0 = tl[ring_idx(lane, c)], a1 = tl[ring_idx(lane + 32, c)];
+        z_t ar0 = a0, ar1 = a1, ac0 = a0, ac1 = a1;
+        if (diag) {  // lower triangle only; the Hermitian diagonal is real
+          ar0 = (lane > c) ? a0 : ((lane == c) ? make_double2(a0.x, 0.0) : zero);
+          ar1 = (lane + 32 > c) ? a1 : ((lane + 32 == c) ? make_double2(a1.x, 0.0) : zero);
+          ac0 = (lane > c) ? a0 : zero;
+          ac1 = (lane + 32 > c) ? a1 : zero;
+        }
+        const z_t vcc = vc[c];
+        zfma(r0, ar0, vcc);
+        zfma(r1, ar1, vcc);
+        pc[cc] = zero;
+        zcfma(pc[cc], ac0, v0);
+        zcfma(pc[cc], ac1, v1);
+      }
+      const z_t ctot = warp_transpose_zsum8(pc);
+      z_t* rowred = swp + (j & 1) * (8 * kT + kT);  // [8 warps][64 rows] | [64 cols]
+      if ((lane & 3) == 0) rowred[8 * kT + 8 * warp + (lane >> 2)] = ctot;
+      rowred[warp * kT + lane] = r0;
+      rowred[warp * kT + lane + 32] = r1;
+      __syncthreads();  // tile k fully read; this tile's partials and the next vectors visible
+      {
+        const int kn = fwd ? k + kRing : k - kRing;  // refill the slot with the tile it serves next
+        if (kn >= 0 && kn < T)
+          ring.issue(k % kRing, &a.tmap, int64_t(sp + (ttab[kn] & 0xffff)) * kT,
+                     int64_t(sp + (ttab[kn] >> 16)) * kT);
+      }
+      if (tid < kT) {
+        z_t sr = rowred[tid];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) sr = zadd(sr, rowred[w * kT + tid]);
+        const z_t sc = rowred[8 * kT + tid];
+        const int gi = sp + bi, gj = sp + bj;
+        if (diag) {
+          a.Y[(int64_t(gi) * a.nch + gi) * kT + tid] = zadd(sr, sc);
+        } else {
+          a.Y[(int64_t(gi) * a.nch + gj) * kT + tid] = sr;
+          a.Y[(int64_t(gj) * a.nch + gi) * kT + tid] = sc;
+        }
+        // v^H (A v) contributions of this tile: rows R (A_t v_C) and, mirrored, cols C
+        vav += zcmul(vrv, sr).x + zcmul(vcv, sc).x;
+      }
+    }
+    {
+      const double vtot = block_sum(vav, dred);
+      if (tid == 0) a.vav[cta] = vtot;
+    }
     // reflector vector into the panels (rows >= g+1 of the owned slabs)
     if (q == 0) {
       for (int c = first_owned(int(g1 / kT), cta, G); c < a.nch; c += G) {
         const int64_t r = int64_t(c) * kT + rl;
         if (r < n && r >= g1) {
-          const z_t v = (r == g1) ? make_double2(1.0, 0.0) : zmul(scale, a.A[r + g * lda]);
+          const z_t v = (r == g1) ? one : zmul(scale, a.A[r + g * lda]);
           V[r + int64_t(i) * ldp] = v;
           a.WV[r + int64_t(NB + i) * ldp] = v;
         }
       }
-    }
-    trace(i, 1);
-    // hemv over lower tiles of the trailing matrix rows/cols [g+1, n)
-    {
-      const int c0 = int(g1 / kT);
-      const int K = a.nch - c0;
-      const int64_t ntiles = int64_t(K) * (K + 1) / 2;
-      double vav = 0.0;
-      for (int64_t tt = cta; tt < ntiles; tt += G) {
-        // alternate the sweep direction every column: the tiles streamed last by column g-1
-        // are still in L2 and are read first here (serpentine order)
-        const int64_t t = (g & 1) ? ntiles - 1 - tt : tt;
-        int bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-        while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
-        while (int64_t(bi) * (bi + 1) / 2 > t) --bi;
-        const int bj = int(t - int64_t(bi) * (bi + 1) / 2);
-        const int64_t R0 = int64_t(c0 + bi) * kT, C0 = int64_t(c0 + bj) * kT;
-        const bool diag = (bi == bj);
-        __syncthreads();
-        // all 16 loads of this thread in flight at once (cp.async, masked entries zero-filled)
-#pragma unroll
-        for (int k = 0; k < kT * kT / kThreads; ++k) {
-          const int e2 = tid + k * kThreads;
-          const int rr = e2 % kT, cc = e2 / kT;
-          const int64_t r = R0 + rr, cl = C0 + cc;
-          const bool ok = r < n && cl < n && cl >= g1 && r >= cl;
-          cp_async16(tile + rr + cc * (kT + 1), ok ? a.A + r + cl * lda : a.A, ok);
-        }
-        cp_async_commit();
-        if (tid < kT) {
-          const int64_t r = R0 + tid;
-          z_t v = zero;
-          if (r == g1) v = make_double2(1.0, 0.0);
-          else if (r > g1 && r < n) v = zmul(scale, a.A[r + g * lda]);
-          vr[tid] = v;
-        } else if (tid < 2 * kT) {
-          const int64_t cl = C0 + (tid - kT);
-          z_t v = zero;
-          if (cl == g1) v = make_double2(1.0, 0.0);
-          else if (cl > g1 && cl < n) v = zmul(scale, a.A[cl + g * lda]);
-          vc[tid - kT] = v;
-        }
-        cp_async_wait<0>();
-        __syncthreads();
-        if (diag && tid < kT) tile[tid + tid * (kT + 1)].y = 0.0;  // Hermitian diagonal is real
-        if (diag) __syncthreads();
-        z_t yr = zero, yc = zero;
-#pragma unroll 4
-        for (int k = q * (kT / kQ); k < (q + 1) * (kT / kQ); ++k) {
-          zfma(yr, tile[rl + k * (kT + 1)], vc[k]);
-          if (!diag || k > rl) zcfma(yc, tile[k + rl * (kT + 1)], vr[k]);
-        }
-        red[q * kT + rl] = yr;
-        red2[q * kT + rl] = yc;
-        __syncthreads();
-        if (q == 0) {
-          z_t sr = red[rl], sc = red2[rl];
-#pragma unroll
-          for (int qq = 1; qq < kQ; ++qq) {
-            sr = zadd(sr, red[qq * kT + rl]);
-            sc = zadd(sc, red2[qq * kT + rl]);
-          }
-          const int gi = c0 + bi, gj = c0 + bj;
-          if (diag) {
-            a.Y[(int64_t(gi) * a.nch + gi) * kT + rl] = zadd(sr, sc);
-          } else {
-            a.Y[(int64_t(gi) * a.nch + gj) * kT + rl] = sr;
-            a.Y[(int64_t(gj) * a.nch + gi) * kT + rl] = sc;
-          }
-          // v^H (A v) contributions of this tile: rows R (A_t v_C) and, mirrored, cols C
-          const z_t cr = zcmul(vr[rl], sr), cc2 = zcmul(vc[rl], sc);
-          vav += cr.x + cc2.x;
-        }
-      }
-      const double vtot = block_sum(vav, dred);
-      if (tid == 0) a.vav[cta] = vtot;
     }
     if (cta == G - 1) {  // the last CTA has the fewest tiles: t1/t2 off the critical path
       // t1 = W^H v, t2 = V^H v over rows >= g+1 (v(g+1) = 1, v(r) = scale x(r))
       const int kk = tid >> 2, part = tid & 3;  // 64 sums x 4 partial lanes
       const int p = kk & (NB - 1);
       z_t s = zero;
-      if (p < i) s = zsum_strided(a.s12p + kk, 2 * NB, int(g / kT) + part, a.nch, 4);
+      if (p < i) s = zsum_strided16(a.s12p + kk, 2 * NB, int(g / kT) + part, a.nch, 4);
       s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
       s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
       s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
@@ -309,63 +351,73 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
     grid.sync();
     trace(i, 3);
     // ---------------------------------------------------------------- phase B
-    if (warp == 0) {
-      const double vw0 = warp_sum_range(a.vav, 0, G);
-      if (lane == 0) dred[1] = vw0;
-    }
-    if (tid >= 64 && tid < 64 + 2 * NB) tt[tid - 64] = a.t12[tid - 64];  // zero beyond i
-    __syncthreads();
-    const double vav = dred[1];
-    // v^H w' = v^H A v - sum_p [conj(t2_p) t1_p + conj(t1_p) t2_p]  (real)
-    double vw = vav;
-#pragma unroll
-    for (int p = 0; p < NB; ++p) {
-      if (p < i) {
-        const z_t c = zcmul(tt[NB + p], tt[p]);
-        vw -= 2.0 * c.x;
-      }
-    }
-    const double tau2 = zabs2(tau);
-    const double alw = -0.5 * tau2 * vw;  // alpha of W = tau w' + alpha v (real)
     const int c0 = int(g1 / kT);
-    // row g+1 of V and W (W(g+1, i) redundantly in every CTA, fixed order)
-    if (warp == 0) {
-      const int cg1 = int(g1 / kT), off = int(g1 % kT);
-      z_t y = zsum_strided(a.Y + int64_t(cg1) * a.nch * kT + off, kT, c0 + lane, a.nch, 32);
-      z_t corr = zero;
-      z_t vgp = zero, wgp = zero;
-      if (lane < i) {
-        vgp = V[g1 + int64_t(lane) * ldp];
-        wgp = W[g1 + int64_t(lane) * ldp];
-        corr = zadd(zmul(vgp, tt[lane]), zmul(wgp, tt[NB + lane]));
-      }
-      y = warp_zsum(y);
-      corr = warp_zsum(corr);
-      if (lane < NB) {
-        vg[lane] = lane < i ? vgp : (lane == i ? make_double2(1.0, 0.0) : zero);
-        wg[lane] = lane < i ? wgp : zero;
-      }
-      if (lane == 0) wg[i] = make_double2(zmul(tau, zsub(y, corr)).x + alw,
-                                         zmul(tau, zsub(y, corr)).y);
-    }
-    __syncthreads();
-    for (int c = first_owned(c0, cta, G); c < a.nch; c += G) {
+    double alw = 0.0;  // alpha of W (register: block_sum below reuses dred)
+    for (int c = first_owned(c0, cta, G), first = 1; c < a.nch; c += G, first = 0) {
       const int64_t r = int64_t(c) * kT + rl;
       const bool valid = r < n && r >= g1;
-      z_t ypart = zero, upd = zero, vri = zero, xold = zero;
-      if (valid) {
-        if (q == 0) {
-          vri = V[r + int64_t(i) * ldp];
-          if (has_next) xold = a.A[r + g1 * lda];
+      // every load of the phase is issued before the first consumer
+      z_t vrr[NB / kQ], wrr[NB / kQ], vri = zero, xold = zero, ypart = zero;
+      double vw0 = 0.0;
+      z_t ysum = zero, vgp = zero, wgp = zero, tpre = zero;
+      if (first) {
+        if (warp == 0) {
+          vw0 = warp_sum_range(a.vav, 0, G);
+          ysum = zsum_strided16(a.Y + int64_t(c0) * a.nch * kT + (g1 % kT), kT, c0 + lane, a.nch, 32);
+          if (lane < i) {
+            vgp = V[g1 + int64_t(lane) * ldp];
+            wgp = W[g1 + int64_t(lane) * ldp];
+          }
         }
-        ypart = zsum_strided(a.Y + int64_t(c) * a.nch * kT + rl, kT, c0 + q, a.nch, kQ);
+        if (tid >= 64 && tid < 64 + 2 * NB) tpre = a.t12[tid - 64];  // zero beyond i
+      }
+#pragma unroll
+      for (int k = 0; k < NB / kQ; ++k) {
+        const int p = q + k * kQ;
+        vrr[k] = (valid && p < i) ? V[r + int64_t(p) * ldp] : zero;
+        wrr[k] = (valid && p < i) ? W[r + int64_t(p) * ldp] : zero;
+      }
+      if (valid) {
+        vri = V[r + int64_t(i) * ldp];
+        if (has_next && q == 0) xold = a.A[r + g1 * lda];
+        ypart = zsum_strided16(a.Y + int64_t(c) * a.nch * kT + rl, kT, c0 + q, a.nch, kQ);
+      }
+      if (first) {
+        if (tid >= 64 && tid < 64 + 2 * NB) tt[tid - 64] = tpre;
+        __syncthreads();
+        if (warp == 0) {  // row g+1 of V and W; alpha of W (same fixed order in every CTA)
+          z_t corr = zero;
+          double vt = 0.0;
+          if (lane < i) {
+            corr = zadd(zmul(vgp, tt[lane]), zmul(wgp, tt[NB + lane]));
+            vt = zcmul(tt[NB + lane], tt[lane]).x;
+          }
+          const z_t y = warp_zsum(ysum);
+          corr = warp_zsum(corr);
+          // v^H w' = v^H A v - sum_p [conj(t2_p) t1_p + conj(t1_p) t2_p]  (real)
+          const double vw = vw0 - 2.0 * warp_sum(vt);
+          const double alw0 = -0.5 * zabs2(tau) * vw;  // alpha of W = tau w' + alpha v (real)
+          if (lane < NB) {
+            vg[lane] = lane < i ? vgp : (lane == i ? one : zero);
+            wg[lane] = lane < i ? wgp : zero;
+          }
+          if (lane == 0) {
+            const z_t tw = zmul(tau, zsub(y, corr));
+            wg[i] = make_double2(tw.x + alw0, tw.y);
+            dred[1] = alw0;
+          }
+        }
+        __syncthreads();
+        alw = dred[1];
+      }
+      z_t upd = zero;
+      if (valid) {
 #pragma unroll
         for (int k = 0; k < NB / kQ; ++k) {
           const int p = q + k * kQ;
           if (p < i) {
-            const z_t vrp = V[r + int64_t(p) * ldp], wrp = W[r + int64_t(p) * ldp];
-            ypart = zsub(ypart, zadd(zmul(vrp, tt[p]), zmul(wrp, tt[NB + p])));
-            upd = zadd(upd, zadd(zmul(vrp, zconj(wg[p])), zmul(wrp, zconj(vg[p]))));
+            ypart = zsub(ypart, zadd(zmul(vrr[k], tt[p]), zmul(wrr[k], tt[NB + p])));
+            upd = zadd(upd, zadd(zmul(vrr[k], zconj(wg[p])), zmul(wrr[k], zconj(vg[p]))));
           }
         }
       }
@@ -405,30 +457,25 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
       if (has_next) {
         const double nrm = block_sum(q == 0 ? zabs2(xn) : 0.0, dred);  // syncs: xs, wc visible
         if (tid == 0) a.normp[c] = nrm;
-        // s1[p] = sum conj(W(r,p)) x(r), s2[p] = sum conj(V(r,p)) x(r), p <= i, over the slab
+        // s1[p] = sum conj(W(r,p)) x(r), s2[p] = sum conj(V(r,p)) x(r), p <= i, over the slab,
+        // from the rows held in registers
+        const z_t xv = xs[rl], wci = wc[rl];
+        z_t pr[16];
 #pragma unroll
-        for (int k = 0; k < NB / 8; ++k) {
-          const int p = warp + 8 * k;
-          if (p <= i) {
-            z_t s1 = zero, s2 = zero;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = lane + 32 * h;
-              const int64_t rr = int64_t(c) * kT + j;
-              if (rr < n) {
-                const z_t xv = xs[j];
-                const z_t wv = (p == i) ? wc[j] : W[rr + int64_t(p) * ldp];
-                zcfma(s1, wv, xv);
-                zcfma(s2, V[rr + int64_t(p) * ldp], xv);
-              }
-            }
-            s1 = warp_zsum(s1);
-            s2 = warp_zsum(s2);
-            if (lane == 0) {
-              a.s12p[int64_t(c) * 2 * NB + p] = s1;
-              a.s12p[int64_t(c) * 2 * NB + NB + p] = s2;
-            }
-          }
+        for (int k = 0; k < NB / kQ; ++k) {
+          const int p = q + k * kQ;
+          pr[k] = zero;
+          pr[8 + k] = zero;
+          zcfma(pr[k], (p == i) ? wci : wrr[k], xv);
+          zcfma(pr[8 + k], (p == i) ? vri : vrr[k], xv);
+        }
+        const z_t tot = warp_transpose_zsum16(pr);
+        const int idx = lane >> 1;
+        if ((warp & 1) && !(lane & 1)) red[q * 16 + idx] = tot;  // rows 32..63 of the slab
+        __syncthreads();
+        if (!(warp & 1) && !(lane & 1)) {
+          const int p = q + (idx & 7) * kQ;
+          if (p <= i) a.s12p[int64_t(c) * 2 * NB + (idx >> 3) * NB + p] = zadd(tot, red[q * 16 + idx]);
         }
       }
       __syncthreads();
@@ -437,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2) hetrd_panel_kernel(HetrdArgs a) {
     if (has_next) grid.sync();
     trace(i, 5);
   }
+  ring.drain();  // no TMA load may be in flight when the CTA exits
 }
 
 __global__ void set_last_diag_kernel(const z_t* A, int64_t lda, int64_t n, double* d) {
@@ -460,6 +508,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   z_t* base = reinterpret_cast<z_t*>(ws);
   HetrdArgs a{};
   a.A = A; a.lda = lda; a.n = n; a.d = d; a.e = e; a.tau = tau;
+  a.tmap = make_tile_map(A, lda, n);
   a.ldp = n;
   a.VW = base; base += n * 2 * NB;
   a.WV = base; base += n * 2 * NB;
@@ -470,8 +519,9 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   a.vav = a.normp + nch;
   a.nch = nch;
 
-  const size_t smem = (size_t(kT) * (kT + 1) + 2 * kT + 2 * kQ * kT + 2 * NB + 2 * kT + 2 * NB + 8) *
-                          sizeof(z_t) + 8 * sizeof(double);
+  const size_t smem = (size_t(kRing) * kRingT * kRingT + kRing + 4 * kT + 2 * (8 * kT + kT) + 2 * NB +
+                       2 * kT + 2 * NB + 8) * sizeof(z_t) + kTabMax * sizeof(int) + 8 * sizeof(double) +
+                      128;
   static int blocks_per_sm = -1;
   static int num_sms = 0;
   if (blocks_per_sm < 0) {
@@ -503,6 +553,11 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     const int64_t tiles = ceil_div(m, kT) * (ceil_div(m, kT) + 1) / 2;
     int G = int(min64(min64(int64_t(blocks_per_sm) * num_sms, 4096), tiles));
     G = max(G, 1);
+    {
+      const int64_t K = nch - (p0 + 1) / kT;
+      if (ceil_div(K * (K + 1) / 2, int64_t(G)) > kTabMax)
+        throw std::runtime_error("hetrd: matrix too large for the per-CTA tile list");
+    }
     void* args[] = {&a};
     double bytes = 0.0;  // algorithmic: lower triangle of each column's trailing matrix
     for (int i = 0; i < nbp; ++i) {

@@ -4,16 +4,13 @@
 // Used by the cooperative panel kernels (hetrd.cu, gebrd.cu): within one panel the trailing
 // block is read-only, so each CTA streams its fixed list of tiles through kSlots slots, and a
 // tile left in a slot at the end of one mat-vec sweep is reused by the next sweep without a
-// reload. One thread issues eight 2-D TMA boxes per tile; the other threads spend no
-// instructions on the stream.
+// reload. One thread issues one 2-D TMA box per tile; the other threads spend no instructions
+// on the stream.
 //
 // The tensor map views the column-major complex matrix as FLOAT64 [2n x n] (lda*16-byte column
-// stride) with a 16 x 64 box (8 complex rows x 64 columns = 8 KB) and the 128-byte swizzle. A
-// slot holds 8 such boxes; element (row r, col c) of the tile sits at
-//   (r / 8) * 512 + c * 8 + ((r % 8) ^ (c % 8))            [in complex elements]
-// so a warp reading a column (fixed c) or a row (fixed r) hits 8 distinct 16-byte bank groups
-// per 8 lanes: conflict-free in both orientations. Elements outside the matrix are zero-filled
-// by the TMA unit.
+// stride) with a 128 x 64 box: a slot holds the tile column-major and dense, element (r, c) at
+// c * 64 + r, every column a contiguous 1 KB run in global memory and in the slot. The kernels
+// read it with lanes along r (conflict-free). Elements outside the matrix are zero-filled.
 #pragma once
 
 #include <cuda.h>
@@ -24,9 +21,7 @@ namespace bseg {
 
 constexpr int kRingT = 64;  // tile edge
 
-__device__ __forceinline__ int ring_idx(int r, int c) {
-  return (r >> 3) * 512 + c * 8 + ((r & 7) ^ (c & 7));
-}
+__device__ __forceinline__ int ring_idx(int r, int c) { return c * kRingT + r; }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -64,7 +59,7 @@ CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n);
 
 template <int kSlots>
 struct TileRing {
-  z_t* buf;          // kSlots * 64 * 64, 1024-byte aligned
+  z_t* buf;          // kSlots * 64 * 64, 128-byte aligned
   uint64_t* bars;    // kSlots mbarriers
   uint32_t pending;  // slot s has a load not yet waited for (identical in every thread)
   uint32_t phase;    // parity of the next completion of slot s
@@ -82,15 +77,14 @@ struct TileRing {
   }
   __device__ const z_t* slot(int s) const { return buf + s * kRingT * kRingT; }
 
-  // All threads call (bookkeeping); thread 0 issues the 8 boxes of the tile with top-left
-  // element (R0, C0). The slot must be free (a CTA barrier since its last reader).
+  // All threads call (bookkeeping); thread 0 issues the box of the tile with top-left element
+  // (R0, C0). The slot must be free (a CTA barrier since its last reader).
   __device__ void issue(int s, const CUtensorMap* map, int64_t R0, int64_t C0) {
     pending |= 1u << s;
     if (threadIdx.x != 0) return;
     z_t* dst = buf + s * kRingT * kRingT;
     mbar_arrive_expect_tx(&bars[s], kRingT * kRingT * 16u);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 512, map, int(2 * (R0 + 8 * b)), int(C0), &bars[s]);
+    tma_load_2d(dst, map, int(2 * R0), int(C0), &bars[s]);
   }
   // All threads: make slot s readable (waits only if a load is outstanding).
   __device__ void acquire(int s) {
