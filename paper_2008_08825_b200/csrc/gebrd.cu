@@ -388,17 +388,16 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
     __syncthreads();
     const double xn2 = dred[0];
     const z_t alpha = xc[0];
-    __syncthreads();
     double beta;
     z_t tq, scale;
     larfg_params2(alpha, xn2, beta, tq, scale);
-    if (cta == 0) {
-      if (tid == 0) {
-        a.d[g] = beta;
-        a.tauq[g] = tq;
-      }
-      gb_tsum(a.s12, 2 * kNB, 0, s0, a.nch, V + g, ldp, i, scale, t1, kNB);
-      gb_tsum(a.s12, 2 * kNB, kNB, s0, a.nch, X + g, ldp, i, scale, t2, kNB);
+    const bool has_cols = (g + 1 < n);
+    if (has_cols) gb_sweep<true>(a, ring, ttab, vbuf, swp, T, true, g, scale);
+    // off the sweep's critical path: d/tau, the reflector into the panel, t1/t2 (by the CTA
+    // with the fewest tiles)
+    if (cta == 0 && tid == 0) {
+      a.d[g] = beta;
+      a.tauq[g] = tq;
     }
     if (q == 0) {
       for (int c = gb_first_owned(s0, cta, G); c < a.nch; c += G) {
@@ -407,8 +406,10 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
           V[r + int64_t(i) * ldp] = (r == g) ? make_double2(1.0, 0.0) : zmul(scale, a.A[r + g * lda]);
       }
     }
-    const bool has_cols = (g + 1 < n);
-    if (has_cols) gb_sweep<true>(a, ring, ttab, vbuf, swp, T, true, g, scale);
+    if (cta == G - 1) {
+      gb_tsum(a.s12, 2 * kNB, 0, s0, a.nch, V + g, ldp, i, scale, t1, kNB);
+      gb_tsum(a.s12, 2 * kNB, kNB, s0, a.nch, X + g, ldp, i, scale, t2, kNB);
+    }
     trace(i, 3);
     grid.sync();
     trace(i, 4);
@@ -524,15 +525,15 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
       __syncthreads();
       const double xr2 = dred[0];
       const z_t alpha2 = xc[0];
-      __syncthreads();
       double beta2;
       z_t tp, scale2;
       larfg_params2(alpha2, xr2, beta2, tp, scale2);
-      if (cta == 0) {
-        if (tid == 0) {
-          a.e[g] = beta2;
-          a.taup[g] = tp;
-        }
+      gb_sweep<false>(a, ring, ttab, vbuf, swp, T, false, g, scale2);
+      if (cta == 0 && tid == 0) {
+        a.e[g] = beta2;
+        a.taup[g] = tp;
+      }
+      if (cta == G - 1) {
         gb_tsum(a.s34, 2 * (kNB + 1), 0, c0, a.nch, Y + (g + 1), ldp, i + 1, scale2, t3, kNB + 1);
         gb_tsum(a.s34, 2 * (kNB + 1), kNB + 1, c0, a.nch, U + (g + 1), ldp, i, scale2, t4, kNB + 1);
       }
@@ -549,7 +550,6 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
           }
         }
       }
-      gb_sweep<false>(a, ring, ttab, vbuf, swp, T, false, g, scale2);
     }
     trace(i, 7);
     grid.sync();

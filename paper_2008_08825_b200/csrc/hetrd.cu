@@ -358,12 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = r < n && r >= g1;
       // every load of the phase is issued before the first consumer
       z_t vrr[NB / kQ], wrr[NB / kQ], vri = zero, xold = zero, ypart = zero;
-      double vw0 = 0.0;
-      z_t ysum = zero, vgp = zero, wgp = zero, tpre = zero;
+      // warp 0 (first slab): raw terms of v^H A v (G <= 256 per-CTA partials) and of
+      // y(g+1) (chunk partials c0 + lane + 32u), summed after the barrier
+      double vavr[8];
+      z_t ysr[8], vgp = zero, wgp = zero, tpre = zero;
+      const z_t* yrow = a.Y + int64_t(c0) * a.nch * kT + (g1 % kT);
       if (first) {
         if (warp == 0) {
-          vw0 = warp_sum_range(a.vav, 0, G);
-          ysum = zsum_strided16(a.Y + int64_t(c0) * a.nch * kT + (g1 % kT), kT, c0 + lane, a.nch, 32);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            vavr[u] = (lane + 32 * u < G) ? a.vav[lane + 32 * u] : 0.0;
+            const int m = c0 + lane + 32 * u;
+            ysr[u] = (m < a.nch) ? yrow[int64_t(m) * kT] : zero;
+          }
           if (lane < i) {
             vgp = V[g1 + int64_t(lane) * ldp];
             wgp = W[g1 + int64_t(lane) * ldp];
@@ -392,6 +399,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             corr = zadd(zmul(vgp, tt[lane]), zmul(wgp, tt[NB + lane]));
             vt = zcmul(tt[NB + lane], tt[lane]).x;
           }
+          double vs = 0.0;
+          z_t ysum = zero;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            vs += vavr[u];
+            ysum = zadd(ysum, ysr[u]);
+          }
+          for (int m = c0 + lane + 256; m < a.nch; m += 32) ysum = zadd(ysum, yrow[int64_t(m) * kT]);
+          const double vw0 = warp_sum(vs);
           const z_t y = warp_zsum(ysum);
           corr = warp_zsum(corr);
           // v^H w' = v^H A v - sum_p [conj(t2_p) t1_p + conj(t1_p) t2_p]  (real)
@@ -551,7 +567,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     // shrink the grid with the trailing size (fewer CTAs => cheaper grid barriers)
     const int64_t m = n - p0;
     const int64_t tiles = ceil_div(m, kT) * (ceil_div(m, kT) + 1) / 2;
-    int G = int(min64(min64(int64_t(blocks_per_sm) * num_sms, 4096), tiles));
+    int G = int(min64(min64(int64_t(blocks_per_sm) * num_sms, 256), tiles));  // phase B: G <= 256
     G = max(G, 1);
     {
       const int64_t K = nch - (p0 + 1) / kT;
