@@ -5,6 +5,9 @@
 // and cblas_zgemm (backend.cpp:170-173).
 #include "blas.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <cudaTypedefs.h>
 
 #include "tile_ring.cuh"
@@ -101,6 +104,11 @@ void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_
     ksplit = max(1, min(ksplit, 32));
     while (ksplit > 1 && int64_t(ksplit) * m * n > ws_elems) --ksplit;
   }
+  static const bool log = getenv("BSE_GEMM_LOG") != nullptr;  // developer shape log
+  if (log)
+    fprintf(stderr, "zgemm %lld %lld %lld op%d%d sh%d%d cl%d ks%d gflop %.3f\n", (long long)m,
+            (long long)n, (long long)k, opa, opb, a_shape, b_shape, c_lower, ksplit,
+            1e-9 * zgemm_exec_flops(m, n, k, a_shape, b_shape, c_lower));
   if (ksplit > 1) {
     p.ksplit = ksplit;
     p.P = ws;
@@ -126,6 +134,9 @@ void zgemm_batched(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64
   p.alpha = alpha; p.beta = beta;
   p.sA = sA; p.sB = sB; p.sC = sC;
   p.ksplit = 1;
+  if (getenv("BSE_GEMM_LOG"))
+    fprintf(stderr, "zgemm %lld %lld %lld op%d%d batch%d gflop %.3f\n", (long long)m, (long long)n,
+            (long long)k, opa, opb, batch, 8e-9 * double(m) * double(n) * double(k) * batch);
   launch_z_any(s, opa, opb, p,
                dim3(unsigned(ceil_div(m, kBM)), unsigned(ceil_div(n, kBN)), unsigned(batch)));
 }

@@ -209,26 +209,45 @@ __global__ void __launch_bounds__(ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, 
   }
   cp_async_wait<0>();
 
-  // Epilogue.
+  // Epilogue. The C reads of a row pair are issued before any store (stores to C could alias
+  // later reads, so the compiler cannot hoist loads over them): 2 memory round trips per tile
+  // instead of one per element, which dominates short-K products (k = 64 trailing updates).
+  const bool use_beta = p.ksplit == 1 && (p.beta.x != 0.0 || p.beta.y != 0.0);
 #pragma unroll
-  for (int a = 0; a < T::MT; ++a)
+  for (int a0 = 0; a0 < T::MT; a0 += 2) {
+    z_t cv[2][T::NT][2];
 #pragma unroll
-    for (int b = 0; b < T::NT; ++b)
+    for (int da = 0; da < 2; ++da)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t gi = m0 + wm0 + a * 8 + fr;
-        const int64_t gj = n0 + wn0 + b * 8 + 2 * fk + h;
-        if (gi >= p.m || gj >= p.n) continue;
-        const z_t acc = make_double2(acc_re[a][b][h], acc_im[a][b][h]);
-        if (p.ksplit > 1) {
-          p.P[int64_t(split) * p.m * p.n + gi + gj * p.m] = acc;
-          continue;
+      for (int b = 0; b < T::NT; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t gi = m0 + wm0 + (a0 + da) * 8 + fr;
+          const int64_t gj = n0 + wn0 + b * 8 + 2 * fk + h;
+          const bool live = use_beta && gi < p.m && gj < p.n && !(p.c_lower && gi < gj);
+          cv[da][b][h] = live ? C[gi + gj * p.ldc] : make_double2(0.0, 0.0);
         }
-        if (p.c_lower && gi < gj) continue;
-        z_t out = zmul(p.alpha, acc);
-        if (p.beta.x != 0.0 || p.beta.y != 0.0) out = zadd(out, zmul(p.beta, C[gi + gj * p.ldc]));
-        C[gi + gj * p.ldc] = out;
-      }
+#pragma unroll
+    for (int da = 0; da < 2; ++da)
+#pragma unroll
+      for (int b = 0; b < T::NT; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = a0 + da;
+          const int64_t gi = m0 + wm0 + a * 8 + fr;
+          const int64_t gj = n0 + wn0 + b * 8 + 2 * fk + h;
+          if (gi >= p.m || gj >= p.n) continue;
+          const z_t acc = make_double2(acc_re[a][b][h], acc_im[a][b][h]);
+          if (p.ksplit > 1) {
+            p.P[int64_t(split) * p.m * p.n + gi + gj * p.m] = acc;
+            continue;
+          }
+          if (p.c_lower && gi < gj) continue;
+          z_t out = zmul(p.alpha, acc);
+          if (use_beta) out = zadd(out, zmul(p.beta, cv[da][b][h]));
+          C[gi + gj * p.ldc] = out;
+        }
+  }
 }
 
 // Reduces K-split partials: C = alpha * sum_s P_s + beta * C.
