@@ -99,10 +99,20 @@ void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_
   const int64_t tiles_m = ceil_div(m, kBM), tiles_n = ceil_div(n, kBN);
   int ksplit = 1;
   // Under-filled grid with a long K: split K across CTAs (deterministic two-pass reduce).
-  if (ws && tiles_m * tiles_n < 148 && k >= 8 * kBK * 4) {
-    ksplit = int(min64(ceil_div(2 * 148, tiles_m * tiles_n), k / (kBK * 16)));
-    ksplit = max(1, min(ksplit, 32));
-    while (ksplit > 1 && int64_t(ksplit) * m * n > ws_elems) --ksplit;
+  // The split maximises the occupancy of the last wave (2 resident CTAs per SM), with a 1%
+  // per-slice penalty for the extra reduction traffic, and keeps >= 16 k-tiles per slice.
+  const int64_t tiles = tiles_m * tiles_n, slots = 2 * 148;
+  if (ws && tiles < slots && k >= 8 * kBK * 4) {
+    double best = double(tiles) / double(slots);
+    for (int ks = 2; ks <= 32 && int64_t(ks) * kBK * 16 <= k; ++ks) {
+      if (int64_t(ks) * m * n > ws_elems) break;
+      const int64_t ctas = tiles * ks;
+      const double eff = double(ctas) / double(ceil_div(ctas, slots) * slots) * (1.0 - 0.01 * ks);
+      if (eff > best + 1e-9) {
+        best = eff;
+        ksplit = ks;
+      }
+    }
   }
   static const bool log = getenv("BSE_GEMM_LOG") != nullptr;  // developer shape log
   if (log)
