@@ -36,5 +36,6 @@ SvdTriple svd(const Matrix& m);                 // backend.cpp:64-86
 Matrix tri_solve(const CholeskyLower& l, const Matrix& rhs, Side side = Side::Left,
                  Op op = Op::None);             // backend.cpp:109-129
 Matrix matmul(const Matrix& a, const Matrix& b, const MatmulOpts& opts = {});  // :131-175
+Matrix hpd_sqrt(const Matrix& m);               // backend.cpp:88-107 (eigendecomposition)
 
 }  // namespace bse

@@ -39,6 +39,8 @@ typedef enum bse_status_code {
   BSE_ERR_SINGULAR_FACTOR = 7,        /* bse::SingularFactor        types.hpp:89-92  */
   BSE_ERR_NON_POSITIVE_SCALE = 8,     /* bse::NonPositiveScale      types.hpp:94-97  */
   BSE_ERR_INVALID_SPEC = 9,           /* bse::InvalidSpec           types.hpp:109-112 */
+  BSE_ERR_ODD_DIMENSION = 10,         /* bse::OddDimension          types.hpp:99-102  */
+  BSE_ERR_LENGTH_MISMATCH = 11,       /* bse::LengthMismatch        types.hpp:104-107 */
   BSE_ERR_CUDA = 20,                  /* device/runtime failure (no reference analogue) */
   BSE_ERR_OUT_OF_MEMORY = 21,
   BSE_ERR_NO_DEVICE = 22
@@ -113,8 +115,10 @@ int bse_abi_version(void);
  *   v              : 2n x n complex, column-major, leading dimension ldv >= 2n
  *   near_singular  : capacity n; receives the flagged (clamped) indices, ascending
  *   n_near_singular: number written
- * method must be BSE_METHOD_CHOL or BSE_METHOD_CHOL_SVD; SQRT / REFERENCE are outside the
- * accelerated scope and return BSE_ERR_INVALID_SPEC ("not accelerated").            */
+ * BSE_METHOD_CHOL and BSE_METHOD_CHOL_SVD are the hot path; BSE_METHOD_SQRT (bse::solve_sqrt,
+ * solvers.cpp:94-117) and BSE_METHOD_REFERENCE (the pencil oracle bse::solve_reference,
+ * solvers.cpp:163-211) are composed from the same device primitives (SURVEY §8f rows f2,
+ * f3). Unknown methods return BSE_ERR_INVALID_SPEC.                                       */
 int bse_solve(bse_ctx* ctx, int method, int64_t n,
               const double* a, int64_t lda, const double* b, int64_t ldb,
               double* lambda, double* v, int64_t ldv,
@@ -164,6 +168,44 @@ int bse_hermitian_eig(bse_ctx* ctx, int64_t n, const double* m, int64_t ldm,
 /* svd (backend.cpp:64-86): zgesvd 'A','A' semantics; s descending; v (not v^H).         */
 int bse_svd(bse_ctx* ctx, int64_t n, const double* m, int64_t ldm,
             double* u, int64_t ldu, double* s, double* v, int64_t ldv, bse_status* st);
+
+/* hpd_sqrt (backend.cpp:88-107): s = m^{1/2} for Hermitian positive definite m (lower
+ * triangle read); BSE_ERR_NOT_POSITIVE_DEFINITE (pivot_index = eigenvalue index) when an
+ * eigenvalue is at or below eps * lambda_max.                                             */
+int bse_hpd_sqrt(bse_ctx* ctx, int64_t n, const double* m, int64_t ldm, double* s, int64_t lds,
+                 bse_status* st);
+
+/* ---------------------------------------------------------------- diagnostics (verify.cpp)
+ * device versions of the reference's checks (DMMA GEMMs + fixed-order
+ * reductions, bit-deterministic). Host-pointer and *_device variants.                    */
+/* residual (verify.cpp:76-93): out[j] = ||H v_j - lambda_j v_j||_2 / ||H||_F, j < k, with
+ * H = [A B; -B -A]; v is 2n x k (ldv >= 2n).                                             */
+int bse_residual(bse_ctx* ctx, int64_t n, const double* a, int64_t lda, const double* b,
+                 int64_t ldb, int64_t k, const double* lambda, const double* v, int64_t ldv,
+                 double* out, bse_status* st);
+int bse_residual_device(bse_ctx* ctx, int64_t n, const double* d_a, int64_t lda,
+                        const double* d_b, int64_t ldb, int64_t k, const double* d_lambda,
+                        const double* d_v, int64_t ldv, double* d_out, bse_status* st);
+/* sigma_orthogonality_error (verify.cpp:70-74): *out = ||V^H Sigma V - I||_F, V rows x k,
+ * rows even (BSE_ERR_ODD_DIMENSION otherwise). *out is a host scalar in both variants.  */
+int bse_sigma_orthogonality_error(bse_ctx* ctx, int64_t rows, int64_t k, const double* v,
+                                  int64_t ldv, double* out, bse_status* st);
+int bse_sigma_orthogonality_error_device(bse_ctx* ctx, int64_t rows, int64_t k,
+                                         const double* d_v, int64_t ldv, double* out,
+                                         bse_status* st);
+/* check_form1 / check_form2 (verify.cpp:46-68): *result = 1 iff J X J = m (X = m^H for form
+ * 1, m^T for form 2) and Sigma m^H Sigma = m within tol * ||m||_F; m is rows x rows.      */
+int bse_check_form(bse_ctx* ctx, int form, int64_t rows, const double* m, int64_t ldm,
+                   double tol, int* result, bse_status* st);
+int bse_check_form_device(bse_ctx* ctx, int form, int64_t rows, const double* d_m, int64_t ldm,
+                          double tol, int* result, bse_status* st);
+/* negative_spectrum (solvers.cpp:223-236): lambda_out = -lambda, v_out = [v_bottom; v_top]. */
+int bse_negative_spectrum(bse_ctx* ctx, int64_t n, int64_t k, const double* lambda,
+                          const double* v, int64_t ldv, double* lambda_out, double* v_out,
+                          int64_t ldvo, bse_status* st);
+int bse_negative_spectrum_device(bse_ctx* ctx, int64_t n, int64_t k, const double* d_lambda,
+                                 const double* d_v, int64_t ldv, double* d_lambda_out,
+                                 double* d_v_out, int64_t ldvo, bse_status* st);
 
 /* ---------------------------------------------------------------- input synthesis
  * Counter-based seeded generators for BASELINE.json configs (host, OpenMP). Each entry

@@ -33,6 +33,9 @@ __all__ = [
     "ConvergenceFailure", "SingularFactor", "NonPositiveScale", "InvalidSpec", "DeviceError",
     "from_blocks", "product_pair", "assemble_eigenvectors", "solve_chol", "solve_chol_svd",
     "solve", "negative_spectrum", "hermitian_eig", "cholesky_lower", "svd", "tri_solve", "matmul",
+    "solve_sqrt", "solve_reference", "hpd_sqrt", "residual", "sigma_orthogonality_error",
+    "check_form1", "check_form2", "check_pairing", "predicted_error", "OddDimension",
+    "LengthMismatch",
     "Context", "default_context", "method_name", "method_from_name", "machine_eps",
     "K_DEFAULT_HERM_TOL",
 ]
@@ -130,6 +133,14 @@ class InvalidSpec(Error):
     pass
 
 
+class OddDimension(Error):
+    """types.hpp:99-102."""
+
+
+class LengthMismatch(Error):
+    """types.hpp:104-107."""
+
+
 class DeviceError(Error):
     """CUDA runtime / no-device failures (no reference analogue)."""
 
@@ -153,6 +164,10 @@ def _raise(st: Status):
         raise NonPositiveScale(msg)
     if c == 9:
         raise InvalidSpec(msg)
+    if c == 10:
+        raise OddDimension(msg)
+    if c == 11:
+        raise LengthMismatch(msg)
     if c in (20, 21, 22):
         raise DeviceError(msg)
     raise Error(msg)
@@ -364,23 +379,110 @@ def solve_chol_svd(h: BseMatrixI, ctx: Optional[Context] = None) -> SpectralResu
     return _solve(Method.CholSvd, h, ctx)
 
 
+def solve_sqrt(h: BseMatrixI, ctx: Optional[Context] = None) -> SpectralResult:
+    """solvers.cpp:94-117 (Algorithm 1, square-root form) on the GPU."""
+    return _solve(Method.Sqrt, h, ctx)
+
+
+def solve_reference(h: BseMatrixI, ctx: Optional[Context] = None) -> SpectralResult:
+    """solvers.cpp:163-211 (Hermitian-definite pencil oracle) on the GPU (§8f row f3)."""
+    return _solve(Method.Reference, h, ctx)
+
+
 def solve(method: Method, h: BseMatrixI, ctx: Optional[Context] = None) -> SpectralResult:
-    """solvers.cpp:213-221. Sqrt / Reference are outside the accelerated scope and raise
-    InvalidSpec (they are never silently computed on the CPU)."""
+    """solvers.cpp:213-221: dispatch over the four methods (all on the GPU)."""
     if int(method) not in (0, 1, 2, 3):
         raise InvalidSpec("unknown method")
     return _solve(Method(method), h, ctx)
 
 
-def negative_spectrum(h: BseMatrixI, r: SpectralResult) -> SpectralResult:
-    """solvers.cpp:223-236: -lambda with halves swapped (pure data movement)."""
+def negative_spectrum(h: BseMatrixI, r: SpectralResult,
+                      ctx: Optional[Context] = None) -> SpectralResult:
+    """solvers.cpp:223-236: -lambda with halves swapped (bse_negative_spectrum)."""
     n = h.n
     if r.v.shape[0] != 2 * n or r.v.shape[1] != r.lambda_.shape[0]:
         raise DimensionMismatch("spectral result does not match the matrix dimension")
-    v = np.empty_like(r.v)
-    v[:n] = r.v[n:]
-    v[n:] = r.v[:n]
-    return SpectralResult(-r.lambda_, v, r.method, list(r.near_singular))
+    ctx = ctx or default_context()
+    k = r.v.shape[1]
+    lam_in = np.ascontiguousarray(r.lambda_, dtype=np.float64)
+    vin = _cm(r.v)
+    lam = np.zeros(k)
+    v = np.zeros((2 * n, k), dtype=np.complex128, order="F")
+    st = Status()
+    _check(_lib.lib().bse_negative_spectrum(ctx.handle, n, k, _p(lam_in), _p(vin), max(2 * n, 1),
+                                            _p(lam), _p(v), max(2 * n, 1), ctypes.byref(st)), st)
+    return SpectralResult(lam, v, r.method, list(r.near_singular))
+
+
+# --------------------------------------------------------------------------- diagnostics (verify.cpp)
+def residual(h: BseMatrixI, r: SpectralResult, ctx: Optional[Context] = None) -> np.ndarray:
+    """verify.cpp:76-93: per-column ||H v_j - lambda_j v_j||_2 / ||H||_F (GPU, §8f row f1)."""
+    ctx = ctx or default_context()
+    n = h.n
+    k = r.v.shape[1]
+    if r.v.shape[0] != 2 * n or r.lambda_.shape[0] != k:
+        raise DimensionMismatch("residual: result does not conform to the matrix")
+    out = np.zeros(k)
+    lam = np.ascontiguousarray(r.lambda_, dtype=np.float64)
+    v = _cm(r.v)
+    st = Status()
+    _check(_lib.lib().bse_residual(ctx.handle, n, _p(h.a), n, _p(h.b), n, k, _p(lam), _p(v),
+                                   2 * n, _p(out), ctypes.byref(st)), st)
+    return out
+
+
+def sigma_orthogonality_error(v, ctx: Optional[Context] = None) -> float:
+    """verify.cpp:70-74: ||V^H Sigma V - I||_F (GPU)."""
+    ctx = ctx or default_context()
+    v = _cm(v)
+    out = ctypes.c_double(0.0)
+    st = Status()
+    _check(_lib.lib().bse_sigma_orthogonality_error(ctx.handle, v.shape[0], v.shape[1], _p(v),
+                                                    max(v.shape[0], 1), ctypes.byref(out),
+                                                    ctypes.byref(st)), st)
+    return out.value
+
+
+def _check_form(form: int, m, tol: float, ctx: Optional[Context]) -> bool:
+    ctx = ctx or default_context()
+    m = _cm(m)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise DimensionMismatch(f"check_form{form}: matrix must be square")
+    res = ctypes.c_int(0)
+    st = Status()
+    _check(_lib.lib().bse_check_form(ctx.handle, form, m.shape[0], _p(m), max(m.shape[0], 1),
+                                     float(tol), ctypes.byref(res), ctypes.byref(st)), st)
+    return bool(res.value)
+
+
+def check_form1(m, tol: float, ctx: Optional[Context] = None) -> bool:
+    """verify.cpp:46-55: J m^H J = m and Sigma m^H Sigma = m within tol * ||m||_F (GPU)."""
+    return _check_form(1, m, tol, ctx)
+
+
+def check_form2(m, tol: float, ctx: Optional[Context] = None) -> bool:
+    """verify.cpp:57-68: J m^T J = m and Sigma m^H Sigma = m within tol * ||m||_F (GPU)."""
+    return _check_form(2, m, tol, ctx)
+
+
+def check_pairing(pos, neg, tol: float) -> bool:
+    """verify.cpp:95-106: sorted(pos) vs sorted(-neg) within tol * max|pos| (host: an
+    O(n log n) sort, no device work)."""
+    pos = np.asarray(pos, dtype=np.float64)
+    neg = np.asarray(neg, dtype=np.float64)
+    if pos.shape != neg.shape:
+        raise LengthMismatch("check_pairing: spectra have different lengths")
+    scale = np.abs(pos).max() if pos.size else 0.0
+    return bool(np.all(np.abs(np.sort(pos) - np.sort(-neg)) <= tol * scale))
+
+
+def predicted_error(norm_h: float, lam: float, s_lambda: float = 1.0, eps: float = None,
+                    squared_method: bool = False) -> float:
+    """verify.cpp:108-114: first-order eigenvalue error model (host scalar formula)."""
+    eps = machine_eps() if eps is None else eps
+    if squared_method:
+        return eps * (norm_h / s_lambda) * min(norm_h / lam, 1.0 / np.sqrt(eps))
+    return eps * norm_h / s_lambda
 
 
 def solve_device(method: Method, n: int, a_ptr: int, b_ptr: int, lam_ptr: int, v_ptr: int,
@@ -413,6 +515,19 @@ def hermitian_eig(m, ctx: Optional[Context] = None) -> HermitianEig:
     _check(_lib.lib().bse_hermitian_eig(ctx.handle, n, _p(m), n, _p(w), _p(vec), n,
                                         ctypes.byref(st)), st)
     return HermitianEig(w, vec)
+
+
+def hpd_sqrt(m, ctx: Optional[Context] = None) -> np.ndarray:
+    """backend.cpp:88-107: Hermitian square root of an HPD matrix (GPU, §8f row f2)."""
+    ctx = ctx or default_context()
+    m = _cm(m)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise DimensionMismatch(f"hpd_sqrt: matrix is {m.shape[0]}x{m.shape[1]}, expected square")
+    n = m.shape[0]
+    out = np.zeros((n, n), dtype=np.complex128, order="F")
+    st = Status()
+    _check(_lib.lib().bse_hpd_sqrt(ctx.handle, n, _p(m), n, _p(out), n, ctypes.byref(st)), st)
+    return out
 
 
 def cholesky_lower(m, ctx: Optional[Context] = None) -> CholeskyLower:

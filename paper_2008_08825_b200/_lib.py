@@ -63,6 +63,25 @@ SYMBOLS = {
                                   ctypes.POINTER(Status)]),
     "bse_svd": (c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_dp, c_i64,
                         ctypes.POINTER(Status)]),
+    "bse_hpd_sqrt": (c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_i64, ctypes.POINTER(Status)]),
+    "bse_residual": (c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp,
+                             ctypes.POINTER(Status)]),
+    "bse_residual_device": (c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_i64, c_i64, c_dp, c_dp,
+                                    c_i64, c_dp, ctypes.POINTER(Status)]),
+    "bse_sigma_orthogonality_error": (c_int, [c_dp, c_i64, c_i64, c_dp, c_i64,
+                                              ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(Status)]),
+    "bse_sigma_orthogonality_error_device": (c_int, [c_dp, c_i64, c_i64, c_dp, c_i64,
+                                                     ctypes.POINTER(ctypes.c_double),
+                                                     ctypes.POINTER(Status)]),
+    "bse_check_form": (c_int, [c_dp, c_int, c_i64, c_dp, c_i64, ctypes.c_double,
+                               ctypes.POINTER(c_int), ctypes.POINTER(Status)]),
+    "bse_check_form_device": (c_int, [c_dp, c_int, c_i64, c_dp, c_i64, ctypes.c_double,
+                                      ctypes.POINTER(c_int), ctypes.POINTER(Status)]),
+    "bse_negative_spectrum": (c_int, [c_dp, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_dp, c_i64,
+                                      ctypes.POINTER(Status)]),
+    "bse_negative_spectrum_device": (c_int, [c_dp, c_i64, c_i64, c_dp, c_dp, c_i64, c_dp, c_dp,
+                                             c_i64, ctypes.POINTER(Status)]),
     "bse_gen_dominant": (c_int, [c_i64, ctypes.c_uint64, c_int, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, c_dp, c_dp]),
     "bse_gen_gaussian_stream": (c_int, [ctypes.c_uint64, ctypes.c_uint64, c_i64, c_dp]),

@@ -1,6 +1,7 @@
 // bse_api.cpp — the C++ drop-in API (include/bse/*.hpp) implemented over the C-ABI
 // (include/bse_gpu.h). Host-side validation (from_blocks, shape checks) mirrors
 // proj/src/core.cpp and backend.cpp; all numerics run in the CUDA library.
+#include <algorithm>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -8,6 +9,7 @@
 
 #include "bse/backend.hpp"
 #include "bse/solvers.hpp"
+#include "bse/verify.hpp"
 #include "bse_gpu.h"
 
 namespace bse {
@@ -36,6 +38,8 @@ thread_local CtxHolder t_ctx;
     case BSE_ERR_SINGULAR_FACTOR: throw SingularFactor(msg);
     case BSE_ERR_NON_POSITIVE_SCALE: throw NonPositiveScale(msg);
     case BSE_ERR_INVALID_SPEC: throw InvalidSpec(msg);
+    case BSE_ERR_ODD_DIMENSION: throw OddDimension(msg);
+    case BSE_ERR_LENGTH_MISMATCH: throw LengthMismatch(msg);
     case BSE_ERR_CUDA:
     case BSE_ERR_OUT_OF_MEMORY:
     case BSE_ERR_NO_DEVICE: throw DeviceError(msg);
@@ -246,17 +250,116 @@ SpectralResult negative_spectrum(const BseMatrixI& h, const SpectralResult& r) {
   if (r.v.rows() != 2 * n || r.v.cols() != Index(r.lambda.size()))
     throw DimensionMismatch("spectral result does not match the matrix dimension");
   SpectralResult out;
+  const Index k = r.v.cols();
   out.lambda.resize(r.lambda.size());
-  for (size_t i = 0; i < r.lambda.size(); ++i) out.lambda[i] = -r.lambda[i];
-  out.v = Matrix(2 * n, r.v.cols());
-  for (Index j = 0; j < r.v.cols(); ++j)
-    for (Index i = 0; i < n; ++i) {
-      out.v(i, j) = r.v(n + i, j);
-      out.v(n + i, j) = r.v(i, j);
-    }
+  out.v = Matrix(2 * n, k);
+  if (k > 0) {
+    bse_status st{};
+    check(bse_negative_spectrum(ctx(), n, k, r.lambda.data(), dp(r.v), 2 * n, out.lambda.data(),
+                                dp(out.v), 2 * n, &st),
+          st);
+  }
   out.method = r.method;
   out.near_singular = r.near_singular;
   return out;
+}
+
+Matrix hpd_sqrt(const Matrix& m) {
+  if (m.rows() != m.cols()) throw DimensionMismatch("hpd_sqrt: expected square");
+  const Index n = m.rows();
+  Matrix s(n, n);
+  bse_status st{};
+  check(bse_hpd_sqrt(ctx(), n, dp(m), n, dp(s), n, &st), st);
+  return s;
+}
+
+// ------------------------------------------------------------------ verify.hpp
+Matrix SignatureOperators::j_times(const Matrix& x) const {
+  Matrix y(x.rows(), x.cols());
+  for (Index j = 0; j < x.cols(); ++j)
+    for (Index i = 0; i < n; ++i) {
+      y(i, j) = x(n + i, j);
+      y(n + i, j) = -x(i, j);
+    }
+  return y;
+}
+Matrix SignatureOperators::times_j(const Matrix& x) const {
+  Matrix y(x.rows(), x.cols());
+  for (Index j = 0; j < n; ++j)
+    for (Index i = 0; i < x.rows(); ++i) {
+      y(i, j) = -x(i, n + j);
+      y(i, n + j) = x(i, j);
+    }
+  return y;
+}
+Matrix SignatureOperators::sigma_times(const Matrix& x) const {
+  Matrix y = x;
+  for (Index j = 0; j < x.cols(); ++j)
+    for (Index i = n; i < 2 * n; ++i) y(i, j) = -y(i, j);
+  return y;
+}
+Matrix SignatureOperators::times_sigma(const Matrix& x) const {
+  Matrix y = x;
+  for (Index j = n; j < 2 * n; ++j)
+    for (Index i = 0; i < x.rows(); ++i) y(i, j) = -y(i, j);
+  return y;
+}
+
+namespace {
+bool check_form(int form, const Matrix& m, double tol) {
+  if (m.rows() != m.cols())
+    throw DimensionMismatch(std::string(form == 1 ? "check_form1" : "check_form2") +
+                            ": matrix must be square");
+  int res = 0;
+  bse_status st{};
+  check(bse_check_form(ctx(), form, m.rows(), dp(m), m.rows() > 0 ? m.rows() : 1, tol, &res, &st),
+        st);
+  return res != 0;
+}
+}  // namespace
+
+bool check_form1(const Matrix& m, double tol) { return check_form(1, m, tol); }
+bool check_form2(const Matrix& m, double tol) { return check_form(2, m, tol); }
+
+double sigma_orthogonality_error(const Matrix& v) {
+  double out = 0.0;
+  bse_status st{};
+  check(bse_sigma_orthogonality_error(ctx(), v.rows(), v.cols(), dp(v), v.rows() > 0 ? v.rows() : 1,
+                                      &out, &st),
+        st);
+  return out;
+}
+
+RealVector residual(const BseMatrixI& h, const SpectralResult& r) {
+  const Index n = h.n(), k = r.v.cols();
+  if (r.v.rows() != 2 * n || Index(r.lambda.size()) != k)
+    throw DimensionMismatch("residual: result does not conform to the matrix");
+  RealVector out(static_cast<size_t>(k));
+  if (k == 0) return out;
+  bse_status st{};
+  check(bse_residual(ctx(), n, dp(h.a()), n, dp(h.b()), n, k, r.lambda.data(), dp(r.v), 2 * n,
+                     out.data(), &st),
+        st);
+  return out;
+}
+
+bool check_pairing(const RealVector& pos, const RealVector& neg, double tol) {
+  if (pos.size() != neg.size()) throw LengthMismatch("check_pairing: spectra have different lengths");
+  RealVector p = pos, m(neg.size());
+  for (size_t i = 0; i < neg.size(); ++i) m[i] = -neg[i];
+  std::sort(p.begin(), p.end());
+  std::sort(m.begin(), m.end());
+  double scale = 0.0;
+  for (double x : pos) scale = std::max(scale, std::fabs(x));
+  for (size_t i = 0; i < p.size(); ++i)
+    if (!(std::fabs(p[i] - m[i]) <= tol * scale)) return false;
+  return true;
+}
+
+double predicted_error(const ErrorModelInput& in, bool squared_method) {
+  if (squared_method)
+    return in.eps * (in.norm_h / in.s_lambda) * std::min(in.norm_h / in.lambda, 1.0 / std::sqrt(in.eps));
+  return in.eps * in.norm_h / in.s_lambda;
 }
 
 }  // namespace bse

@@ -17,6 +17,21 @@
 
 using namespace bseg;
 
+namespace bseg {  // verify.cu
+size_t residual_workspace_bytes(int64_t n, int64_t k);
+void residual_dev(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* B,
+                  int64_t ldb, int64_t k, const double* lam, const z_t* V, int64_t ldv,
+                  double* out, Bump& w);
+size_t sigma_orth_workspace_bytes(int64_t k);
+void sigma_orth_dev(cudaStream_t s, int64_t h, int64_t k, const z_t* V, int64_t ldv,
+                    double* d_out, Bump& w);
+size_t form_workspace_bytes();
+void form_dev(cudaStream_t s, int form, int64_t h, const z_t* M, int64_t ldm, double* d_out,
+              Bump& w);
+void negative_spectrum_dev(cudaStream_t s, int64_t n, int64_t k, const double* lam, const z_t* V,
+                           int64_t ldv, double* lam_out, z_t* Vo, int64_t ldo);
+}  // namespace bseg
+
 namespace bseg {
 
 Bump arena(bse_ctx* c, size_t bytes) {
@@ -143,10 +158,9 @@ void run_solve(bse_ctx* c, int method, int64_t n, const z_t* A, int64_t lda, con
                int64_t ldb, double* lam, z_t* V, int64_t ldv, std::vector<int64_t>& flagged) {
   if (method == BSE_METHOD_CHOL) solve_chol_dev(c, n, A, lda, B, ldb, lam, V, ldv, flagged);
   else if (method == BSE_METHOD_CHOL_SVD) solve_chol_svd_dev(c, n, A, lda, B, ldb, lam, V, ldv, flagged);
-  else if (method == BSE_METHOD_SQRT || method == BSE_METHOD_REFERENCE)
-    throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1,
-                      std::string("method ") + (method == BSE_METHOD_SQRT ? "sqrt" : "reference") +
-                          " is not accelerated (outside the hot-path scope)"};
+  else if (method == BSE_METHOD_SQRT) solve_sqrt_dev(c, n, A, lda, B, ldb, lam, V, ldv, flagged);
+  else if (method == BSE_METHOD_REFERENCE)
+    solve_reference_dev(c, n, A, lda, B, ldb, lam, V, ldv, flagged);
   else throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "unknown method"};
 }
 
@@ -535,6 +549,196 @@ int bse_svd(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* u, int6
     d2h(c, v, ldv, dV2, n, n, n);
     BSE_CUDA(cudaStreamSynchronize(sm));
     if (h != 0) throw DomainError{BSE_ERR_CONVERGENCE_FAILURE, 0, -1, "zgesvd failed to converge"};
+  });
+}
+
+}  // extern "C"
+
+/* ---------------------------------------------------------------- §8f: hpd_sqrt + diagnostics */
+extern "C" {
+
+int bse_hpd_sqrt(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* out, int64_t lds,
+                 bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 1 || ldm < n || lds < n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "hpd_sqrt: bad dimensions"};
+    const size_t nn = size_t(n) * size_t(n);
+    Bump w = arena(c, 2 * nn * sizeof(z_t) + hpd_sqrt_workspace_bytes(n) + 4096);
+    z_t* dM = w.take<z_t>(nn);
+    z_t* dS = w.take<z_t>(nn);
+    h2d(c, dM, n, m, ldm, n, n);
+    hpd_sqrt_dev(c->stream, n, dM, n, dS, n, w);
+    d2h(c, out, lds, dS, n, n, n);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+static void check_residual_dims(int64_t n, int64_t lda, int64_t ldb, int64_t k, int64_t ldv) {
+  if (n < 1 || lda < n || ldb < n || k < 0 || ldv < 2 * n)
+    throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1,
+                      "residual: result does not conform to the matrix"};
+}
+
+int bse_residual_device(bse_ctx* c, int64_t n, const double* d_a, int64_t lda,
+                        const double* d_b, int64_t ldb, int64_t k, const double* d_lambda,
+                        const double* d_v, int64_t ldv, double* d_out, bse_status* st) {
+  return guarded(c, st, [&] {
+    check_residual_dims(n, lda, ldb, k, ldv);
+    Bump w = arena(c, residual_workspace_bytes(n, k));
+    residual_dev(c->stream, n, reinterpret_cast<const z_t*>(d_a), lda,
+                 reinterpret_cast<const z_t*>(d_b), ldb, k, d_lambda,
+                 reinterpret_cast<const z_t*>(d_v), ldv, d_out, w);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bse_residual(bse_ctx* c, int64_t n, const double* a, int64_t lda, const double* b,
+                 int64_t ldb, int64_t k, const double* lambda, const double* v, int64_t ldv,
+                 double* out, bse_status* st) {
+  return guarded(c, st, [&] {
+    check_residual_dims(n, lda, ldb, k, ldv);
+    if (k == 0) return;
+    const size_t nn = size_t(n) * size_t(n), vk = 2 * size_t(n) * size_t(k);
+    Bump w = arena(c, (2 * nn + vk) * sizeof(z_t) + 2 * size_t(k) * sizeof(double) +
+                          residual_workspace_bytes(n, k) + 4096);
+    z_t* dA = w.take<z_t>(nn);
+    z_t* dB = w.take<z_t>(nn);
+    z_t* dV = w.take<z_t>(vk);
+    double* dl = w.take<double>(size_t(k));
+    double* dout = w.take<double>(size_t(k));
+    h2d(c, dA, n, a, lda, n, n);
+    h2d(c, dB, n, b, ldb, n, n);
+    h2d(c, dV, 2 * n, v, ldv, 2 * n, k);
+    BSE_CUDA(cudaMemcpyAsync(dl, lambda, sizeof(double) * size_t(k), cudaMemcpyHostToDevice,
+                             c->stream));
+    residual_dev(c->stream, n, dA, n, dB, n, k, dl, dV, 2 * n, dout, w);
+    BSE_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * size_t(k), cudaMemcpyDeviceToHost,
+                             c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+static int64_t half_dimension(int64_t rows, const char* who) {
+  if (rows % 2 != 0)
+    throw DomainError{BSE_ERR_ODD_DIMENSION, 0, -1, std::string(who) + ": row dimension must be even"};
+  return rows / 2;
+}
+
+int bse_sigma_orthogonality_error_device(bse_ctx* c, int64_t rows, int64_t k, const double* d_v,
+                                         int64_t ldv, double* out, bse_status* st) {
+  return guarded(c, st, [&] {
+    const int64_t h = half_dimension(rows, "sigma_orthogonality_error");
+    if (k < 0 || ldv < rows) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < rows"};
+    *out = 0.0;
+    if (k == 0) return;
+    Bump w = arena(c, sigma_orth_workspace_bytes(k) + 1024);
+    double* d_out = w.take<double>(1);
+    sigma_orth_dev(c->stream, h, k, reinterpret_cast<const z_t*>(d_v), ldv, d_out, w);
+    double sq = 0.0;
+    BSE_CUDA(cudaMemcpyAsync(&sq, d_out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    *out = std::sqrt(sq);
+  });
+}
+
+int bse_sigma_orthogonality_error(bse_ctx* c, int64_t rows, int64_t k, const double* v,
+                                  int64_t ldv, double* out, bse_status* st) {
+  return guarded(c, st, [&] {
+    const int64_t h = half_dimension(rows, "sigma_orthogonality_error");
+    if (k < 0 || ldv < rows) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < rows"};
+    *out = 0.0;
+    if (k == 0) return;
+    const size_t vk = size_t(rows) * size_t(k);
+    Bump w = arena(c, vk * sizeof(z_t) + sigma_orth_workspace_bytes(k) + 4096);
+    z_t* dV = w.take<z_t>(vk);
+    double* d_out = w.take<double>(1);
+    h2d(c, dV, rows, v, ldv, rows, k);
+    sigma_orth_dev(c->stream, h, k, dV, rows, d_out, w);
+    double sq = 0.0;
+    BSE_CUDA(cudaMemcpyAsync(&sq, d_out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    *out = std::sqrt(sq);
+  });
+}
+
+static void form_result(int form, const double* sums, double tol, int* result) {
+  const double norm = std::sqrt(sums[2]);
+  (void)form;
+  *result = (std::sqrt(sums[0]) <= tol * norm && std::sqrt(sums[1]) <= tol * norm) ? 1 : 0;
+}
+
+int bse_check_form_device(bse_ctx* c, int form, int64_t rows, const double* d_m, int64_t ldm,
+                          double tol, int* result, bse_status* st) {
+  return guarded(c, st, [&] {
+    const char* who = form == 2 ? "check_form2" : "check_form1";
+    if (form != 1 && form != 2) throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "form must be 1 or 2"};
+    if (ldm < rows) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, std::string(who) + ": matrix must be square"};
+    const int64_t h = half_dimension(rows, who);
+    Bump w = arena(c, form_workspace_bytes() + 1024);
+    double* d_out = w.take<double>(4);
+    form_dev(c->stream, form, h, reinterpret_cast<const z_t*>(d_m), ldm, d_out, w);
+    double sums[3];
+    BSE_CUDA(cudaMemcpyAsync(sums, d_out, sizeof(sums), cudaMemcpyDeviceToHost, c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    form_result(form, sums, tol, result);
+  });
+}
+
+int bse_check_form(bse_ctx* c, int form, int64_t rows, const double* m, int64_t ldm, double tol,
+                   int* result, bse_status* st) {
+  return guarded(c, st, [&] {
+    const char* who = form == 2 ? "check_form2" : "check_form1";
+    if (form != 1 && form != 2) throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "form must be 1 or 2"};
+    if (ldm < rows) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, std::string(who) + ": matrix must be square"};
+    const int64_t h = half_dimension(rows, who);
+    const size_t mm = size_t(rows) * size_t(rows);
+    Bump w = arena(c, mm * sizeof(z_t) + form_workspace_bytes() + 4096);
+    z_t* dM = w.take<z_t>(mm);
+    double* d_out = w.take<double>(4);
+    if (rows > 0) h2d(c, dM, rows, m, ldm, rows, rows);
+    form_dev(c->stream, form, h, dM, rows, d_out, w);
+    double sums[3];
+    BSE_CUDA(cudaMemcpyAsync(sums, d_out, sizeof(sums), cudaMemcpyDeviceToHost, c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    form_result(form, sums, tol, result);
+  });
+}
+
+int bse_negative_spectrum_device(bse_ctx* c, int64_t n, int64_t k, const double* d_lambda,
+                                 const double* d_v, int64_t ldv, double* d_lambda_out,
+                                 double* d_v_out, int64_t ldvo, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 0 || k < 0 || ldv < 2 * n || ldvo < 2 * n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1,
+                        "spectral result does not match the matrix dimension"};
+    negative_spectrum_dev(c->stream, n, k, d_lambda, reinterpret_cast<const z_t*>(d_v), ldv,
+                          d_lambda_out, reinterpret_cast<z_t*>(d_v_out), ldvo);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bse_negative_spectrum(bse_ctx* c, int64_t n, int64_t k, const double* lambda,
+                          const double* v, int64_t ldv, double* lambda_out, double* v_out,
+                          int64_t ldvo, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 0 || k < 0 || ldv < 2 * n || ldvo < 2 * n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1,
+                        "spectral result does not match the matrix dimension"};
+    if (n == 0 || k == 0) return;
+    const size_t vk = 2 * size_t(n) * size_t(k);
+    Bump w = arena(c, 2 * vk * sizeof(z_t) + 2 * size_t(k) * sizeof(double) + 4096);
+    z_t* dV = w.take<z_t>(vk);
+    z_t* dO = w.take<z_t>(vk);
+    double* dl = w.take<double>(size_t(k));
+    double* dlo = w.take<double>(size_t(k));
+    h2d(c, dV, 2 * n, v, ldv, 2 * n, k);
+    BSE_CUDA(cudaMemcpyAsync(dl, lambda, sizeof(double) * size_t(k), cudaMemcpyHostToDevice,
+                             c->stream));
+    negative_spectrum_dev(c->stream, n, k, dl, dV, 2 * n, dlo, dO, 2 * n);
+    d2h(c, v_out, ldvo, dO, 2 * n, 2 * n, k);
+    BSE_CUDA(cudaMemcpyAsync(lambda_out, dlo, sizeof(double) * size_t(k), cudaMemcpyDeviceToHost,
+                             c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -72,5 +72,14 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
                         int64_t ldb, double* lam, z_t* V, int64_t ldv,
                         std::vector<int64_t>& flagged);
 size_t solve_workspace_bytes(int method, int64_t n);
+// SURVEY §8f rows f2/f3 (extra_solvers.cu)
+void solve_sqrt_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t* B, int64_t ldb,
+                    double* lam, z_t* V, int64_t ldv, std::vector<int64_t>& flagged);
+void solve_reference_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t* B,
+                         int64_t ldb, double* lam, z_t* V, int64_t ldv,
+                         std::vector<int64_t>& flagged);
+size_t hpd_sqrt_workspace_bytes(int64_t n);
+void hpd_sqrt_dev(cudaStream_t s, int64_t n, const z_t* M, int64_t ldm, z_t* S, int64_t lds,
+                  Bump& b);
 
 }  // namespace bseg

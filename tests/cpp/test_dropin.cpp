@@ -1,10 +1,12 @@
 // C++ drop-in check: the reference's test_solvers.cpp cases written against include/bse/*.hpp
 // (same names and exception classes), linked to libbse_b200.so. Exit code = failures.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
 #include "bse/backend.hpp"
 #include "bse/solvers.hpp"
+#include "bse/verify.hpp"
 
 static int failures = 0;
 #define CHECK(c)                                                  \
@@ -67,10 +69,55 @@ int main() {
     const Matrix p = matmul(m, m, {.op_a = Op::Adjoint});
     CHECK(std::abs(p(0, 0) - Complex(5.0)) < 1e-14);
   }
-  try {
-    solve_sqrt(from_blocks(scalar(2.0), scalar(1.0)));
-    CHECK(false);
-  } catch (const InvalidSpec&) {
+  {  // SQRT / REFERENCE (solvers.cpp:94-117, 163-211): lambda = sqrt(3) for (A, B) = (2, 1)
+    const SpectralResult s = solve_sqrt(from_blocks(scalar(2.0), scalar(1.0)));
+    const SpectralResult p = solve_reference(from_blocks(scalar(2.0), scalar(1.0)));
+    CHECK(std::abs(s.lambda[0] - std::sqrt(3.0)) < 1e-14 && s.method == Method::Sqrt);
+    CHECK(std::abs(p.lambda[0] - std::sqrt(3.0)) < 1e-14 && p.method == Method::Reference);
+  }
+  {  // hpd_sqrt (backend.cpp:88-107) and its NotPositiveDefinite payload
+    Matrix m(2, 2);
+    m(0, 0) = 4.0; m(1, 1) = 9.0;
+    const Matrix s = hpd_sqrt(m);
+    CHECK(std::abs(s(0, 0) - Complex(2.0)) < 1e-14 && std::abs(s(1, 1) - Complex(3.0)) < 1e-14);
+    m(1, 1) = -1.0;
+    try {
+      hpd_sqrt(m);
+      CHECK(false);
+    } catch (const NotPositiveDefinite& e) {
+      CHECK(e.pivot_index() == 0);
+    }
+  }
+  {  // verify.hpp on the GPU: residual, Sigma-orthogonality, forms, pairing
+    Matrix a(3, 3), b(3, 3);
+    for (int i = 0; i < 3; ++i) a(i, i) = 2.0 + i;
+    b(0, 1) = b(1, 0) = 0.5;
+    const BseMatrixI h = from_blocks(a, b);
+    const SpectralResult r = solve_chol(h);
+    const RealVector res = residual(h, r);
+    CHECK(res.size() == 3 && *std::max_element(res.begin(), res.end()) < 1e-14);
+    CHECK(sigma_orthogonality_error(r.v) < 1e-13);
+    const SpectralResult neg = negative_spectrum(h, r);
+    CHECK(check_pairing(r.lambda, neg.lambda, 1e-14));
+    Matrix hm(6, 6);
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i) {
+        hm(i, j) = a(i, j);
+        hm(i, j + 3) = b(i, j);
+        hm(i + 3, j) = -b(i, j);
+        hm(i + 3, j + 3) = -a(i, j);
+      }
+    CHECK(check_form1(hm, 1e-14) && check_form2(hm, 1e-14));
+    try {
+      sigma_orthogonality_error(Matrix(3, 1));
+      CHECK(false);
+    } catch (const OddDimension&) {
+    }
+    try {
+      check_pairing(RealVector{1.0}, RealVector{}, 0.0);
+      CHECK(false);
+    } catch (const LengthMismatch&) {
+    }
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures;

@@ -1,0 +1,229 @@
+"""GPU parity for SURVEY §8f: the reference's diagnostics on the device (row f1), solve_sqrt +
+hpd_sqrt (row f2) and the pencil oracle solve_reference (row f3), each against the CPU oracle
+(oracle/, the LAPACK restatement pinned to the reference's KATs) and numpy on the same inputs.
+
+Tolerances: eigenvalues relative 1e-10 vs the oracle's same method (the squared SQRT method on
+well-conditioned config-2 inputs; the direct pencil everywhere); residuals <= 100 n eps;
+diagnostics to 1e-12 relative of numpy's value on the same arrays.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2008_08825_b200 as bse
+from paper_2008_08825_b200 import configs
+from tests.helpers import EPS, norm_h, residual, sigma_orthogonality_error, vector_phase_errors
+
+pytestmark = pytest.mark.gpu
+RNG = np.random.default_rng(2008)
+
+
+def crand(*shape):
+    return RNG.standard_normal(shape) + 1j * RNG.standard_normal(shape)
+
+
+def assert_solution(a, b, r, ref_lam, lam_tol=1e-10):
+    n = a.shape[0]
+    assert r.lambda_.shape == (n,) and r.v.shape == (2 * n, n)
+    assert np.all(np.isfinite(r.lambda_)) and np.all(np.isfinite(r.v))
+    assert np.all(np.diff(r.lambda_) >= 0) and r.lambda_[0] > 0
+    keep = np.setdiff1d(np.arange(n), r.near_singular)
+    res = residual(a, b, r.lambda_[keep], r.v[:, keep])
+    assert res.max() <= 100 * n * EPS, res.max()
+    err = np.max(np.abs(r.lambda_ - ref_lam) / np.abs(ref_lam))
+    assert err <= lam_tol, err
+
+
+# ------------------------------------------------------------------ row f2: SQRT + hpd_sqrt
+@pytest.mark.parametrize("n", [1, 2, 7, 33, 64, 65, 100, 129, 200])
+def test_solve_sqrt_parity(n):
+    a, b = configs.config2(3, n=n)
+    r = bse.solve_sqrt(bse.from_blocks(a, b))
+    lo, vo, nso = oracle.solve("sqrt", a, b)
+    assert r.method == bse.Method.Sqrt
+    assert_solution(a, b, r, lo)
+    assert r.near_singular == list(nso)
+    errs, bounds, sep = vector_phase_errors(r.v, vo, r.lambda_, norm_h(a, b))
+    assert np.all(errs[sep] <= np.maximum(bounds[sep], 1e-10))
+    assert sigma_orthogonality_error(r.v) <= 1e-9
+
+
+def test_solve_sqrt_config1_real():
+    a, b = configs.config1(0)
+    r = bse.solve(bse.Method.Sqrt, bse.from_blocks(a, b))
+    lo, _, _ = oracle.solve("sqrt", a, b)
+    assert_solution(a, b, r, lo)
+
+
+@pytest.mark.parametrize("n", [1, 3, 64, 65, 150])
+def test_hpd_sqrt(n):
+    x = crand(n, n)
+    m = x @ x.conj().T + n * np.eye(n)
+    s = bse.hpd_sqrt(m)
+    assert np.array_equal(s, s.conj().T)  # hermitized exactly (backend.cpp:104-105)
+    assert np.linalg.norm(s @ s - m) <= 100 * n * EPS * np.linalg.norm(m)
+    w = np.linalg.eigvalsh(s)
+    assert w.min() > 0
+    w_ref, q = np.linalg.eigh(m)
+    s_ref = (q * np.sqrt(w_ref)) @ q.conj().T
+    assert np.linalg.norm(s - s_ref) <= 1e3 * n * EPS * np.linalg.norm(s_ref)
+
+
+def test_hpd_sqrt_not_positive_definite():
+    """backend.cpp:93-101: first eigenvalue at or below eps * lambda_max, with its index."""
+    m = np.diag([1.0, 1e-20, 2.0, -1.0]).astype(complex)
+    with pytest.raises(bse.NotPositiveDefinite) as e:
+        bse.hpd_sqrt(m)
+    assert e.value.pivot_index == 0  # ascending eigenvalues: -1 comes first
+    with pytest.raises(bse.NotPositiveDefinite) as e:
+        bse.hpd_sqrt(np.diag([1.0, 1e-20, 2.0]).astype(complex))
+    assert e.value.pivot_index == 0
+
+
+def test_solve_sqrt_error_payloads():
+    # A-B passes the Cholesky certificate but its square root fails (solvers.cpp:96-101)
+    a = np.diag([3.0, 2e-20]).astype(complex)  # A+B = diag(5, 3e-20), A-B = diag(1, 1e-20)
+    b = np.diag([2.0, 1e-20]).astype(complex)
+    with pytest.raises(bse.NotDefinite) as e:
+        bse.solve_sqrt(bse.from_blocks(a, b))
+    assert e.value.which == bse.Block.M2
+    assert str(e.value).startswith("square root of A-B failed")
+    # certificate order: A+B first (core.cpp:89-99)
+    with pytest.raises(bse.NotDefinite) as e:
+        bse.solve_sqrt(bse.from_blocks(np.eye(2), 2 * np.eye(2)))
+    assert e.value.which == bse.Block.M2
+    with pytest.raises(bse.NotDefinite) as e:
+        bse.solve_sqrt(bse.from_blocks(-np.eye(2), 0.5 * np.eye(2)))
+    assert e.value.which == bse.Block.M1
+
+
+# ------------------------------------------------------------------ row f3: pencil oracle
+@pytest.mark.parametrize("n", [1, 2, 7, 33, 64, 65, 100, 129])
+def test_solve_reference_parity(n):
+    a, b = configs.config2(5, n=n)
+    r = bse.solve_reference(bse.from_blocks(a, b))
+    lo, vo, _ = oracle.solve("reference", a, b)
+    assert r.method == bse.Method.Reference and r.near_singular == []
+    assert_solution(a, b, r, lo)
+    errs, bounds, sep = vector_phase_errors(r.v, vo, r.lambda_, norm_h(a, b))
+    assert np.all(errs[sep] <= np.maximum(bounds[sep], 1e-10))
+    # the pencil normalisation: v^H Sigma v = +1 (solvers.cpp:203-208)
+    assert sigma_orthogonality_error(r.v) <= 1e-9
+
+
+def test_reference_agrees_with_chol_and_svd():
+    a, b = configs.config2(11, n=96)
+    h = bse.from_blocks(a, b)
+    lr = bse.solve_reference(h).lambda_
+    for m in (bse.Method.Chol, bse.Method.CholSvd, bse.Method.Sqrt):
+        assert np.max(np.abs(bse.solve(m, h).lambda_ - lr) / lr) <= 1e-10
+
+
+def test_reference_certificates():
+    with pytest.raises(bse.NotDefinite) as e:
+        bse.solve_reference(bse.from_blocks(np.eye(3), 2 * np.eye(3)))
+    assert e.value.which == bse.Block.M2
+
+
+# ------------------------------------------------------------------ row f1: diagnostics
+@pytest.mark.parametrize("n,k", [(1, 1), (5, 3), (64, 64), (65, 40), (130, 130)])
+def test_residual_matches_numpy(n, k):
+    a, b = configs.config2(7, n=n)
+    h = bse.from_blocks(a, b)
+    v = crand(2 * n, k)
+    lam = np.sort(RNG.uniform(0.5, 3.0, k))
+    got = bse.residual(h, bse.SpectralResult(lam, v, bse.Method.Chol, []))
+    hv_top = a @ v[:n] + b @ v[n:]
+    hv_bot = -(b @ v[:n]) - a @ v[n:]
+    want = np.sqrt(np.sum(np.abs(hv_top - lam * v[:n]) ** 2, axis=0) +
+                   np.sum(np.abs(hv_bot - lam * v[n:]) ** 2, axis=0)) / norm_h(a, b)
+    assert np.allclose(got, want, rtol=1e-12, atol=0)
+
+
+def test_residual_of_a_solution():
+    a, b = configs.config2(1, n=120)
+    h = bse.from_blocks(a, b)
+    r = bse.solve_chol(h)
+    res = bse.residual(h, r)
+    assert res.shape == (120,) and res.max() <= 100 * 120 * EPS
+    with pytest.raises(bse.DimensionMismatch):
+        bse.residual(h, bse.SpectralResult(r.lambda_[:3], r.v, r.method, []))
+
+
+@pytest.mark.parametrize("rows,k", [(2, 1), (10, 4), (128, 64), (130, 130)])
+def test_sigma_orthogonality_matches_numpy(rows, k):
+    v = crand(rows, k)
+    h = rows // 2
+    g = v.conj().T @ np.concatenate([v[:h], -v[h:]])
+    want = np.linalg.norm(g - np.eye(k))
+    assert abs(bse.sigma_orthogonality_error(v) - want) <= 1e-12 * want
+
+
+def test_sigma_orthogonality_of_a_solution_and_errors():
+    a, b = configs.config2(2, n=100)
+    r = bse.solve_chol_svd(bse.from_blocks(a, b))
+    assert bse.sigma_orthogonality_error(r.v) <= 1e-10
+    with pytest.raises(bse.OddDimension):
+        bse.sigma_orthogonality_error(crand(5, 2))
+
+
+def test_check_forms():
+    a, b = configs.config2(4, n=40)
+    hm = np.block([[a, b], [-b, -a]])  # H of the residual (verify.cpp:84-86), A, B Hermitian
+    assert bse.check_form1(hm, 1e-12)
+    pert = hm.copy()
+    pert[0, 1] += 1e-3
+    assert not bse.check_form1(pert, 1e-12)
+    # form II uses the transpose in the J condition: a real BSE matrix satisfies both
+    ar, br = configs.config1(0)
+    hr = np.block([[ar, br], [-br, -ar]]).astype(complex)
+    assert bse.check_form1(hr, 1e-12) and bse.check_form2(hr, 1e-12)
+    with pytest.raises(bse.OddDimension):
+        bse.check_form1(crand(3, 3), 1e-12)
+    with pytest.raises(bse.DimensionMismatch):
+        bse.check_form2(crand(4, 2), 1e-12)
+
+
+def test_check_form_matches_reference_formula():
+    """verify.cpp:46-68 restated with numpy on random (non-BSE) matrices near the threshold."""
+    n = 6
+    for trial in range(6):
+        m = crand(2 * n, 2 * n)
+        J = np.block([[np.zeros((n, n)), np.eye(n)], [-np.eye(n), np.zeros((n, n))]])
+        S = np.diag(np.r_[np.ones(n), -np.ones(n)])
+        norm = np.linalg.norm(m)
+        for form, x in ((1, m.conj().T), (2, m.T)):
+            dj = np.linalg.norm(J @ x @ J - m)
+            ds = np.linalg.norm(S @ m.conj().T @ S - m)
+            tol = max(dj, ds) / norm * (1.0 + 1e-9)  # just accepts
+            assert bse._check_form(form, m, tol, None)
+            assert not bse._check_form(form, m, 0.999 * max(dj, ds) / norm, None)
+
+
+def test_negative_spectrum_device():
+    lam = np.array([1.0, 2.0])
+    v = np.arange(8, dtype=complex).reshape(4, 2) * (1 + 0.5j)
+    h = bse.BseMatrixI(np.eye(2, dtype=complex), np.zeros((2, 2), complex))
+    neg = bse.negative_spectrum(h, bse.SpectralResult(lam, v, bse.Method.Chol, [1]))
+    assert np.array_equal(neg.lambda_, -lam)
+    assert np.array_equal(neg.v[:2], v[2:]) and np.array_equal(neg.v[2:], v[:2])
+    assert neg.near_singular == [1] and neg.method == bse.Method.Chol
+
+
+def test_negative_spectrum_of_a_solution_pairs():
+    a, b = configs.config2(9, n=80)
+    h = bse.from_blocks(a, b)
+    r = bse.solve_chol(h)
+    neg = bse.negative_spectrum(h, r)
+    res = bse.residual(h, neg)
+    assert res.max() <= 100 * 80 * EPS
+    assert bse.check_pairing(r.lambda_, neg.lambda_, 1e-14)
+    with pytest.raises(bse.LengthMismatch):
+        bse.check_pairing(r.lambda_, neg.lambda_[:3], 1e-14)
+
+
+def test_predicted_error_formula():
+    """verify.cpp:108-114."""
+    e = bse.machine_eps()
+    assert bse.predicted_error(10.0, 0.5, 0.5) == e * 10.0 / 0.5
+    assert bse.predicted_error(10.0, 0.5, 0.5, squared_method=True) == e * 20.0 * min(20.0, 1 / np.sqrt(e))

@@ -309,11 +309,14 @@ def test_breakdown_regime_gpu():
     assert np.all(rc.lambda_ >= EPS * rc.lambda_[-1] * (1 - 1e-12))
 
 
-def test_unaccelerated_methods_refuse():
+def test_all_methods_dispatch():
+    """solvers.cpp:213-221: every method runs (SQRT / REFERENCE composed on the GPU, §8f)."""
     h = bse.from_blocks(np.array([[2.0]]), np.array([[1.0]]))
-    for m in (bse.Method.Sqrt, bse.Method.Reference):
-        with pytest.raises(bse.InvalidSpec):
-            bse.solve(m, h)
+    for m in (bse.Method.Sqrt, bse.Method.Chol, bse.Method.CholSvd, bse.Method.Reference):
+        r = bse.solve(m, h)
+        assert abs(r.lambda_[0] - np.sqrt(3.0)) <= 1e-14 and r.method == m
+    with pytest.raises(bse.InvalidSpec):
+        bse.solve(7, h)
 
 
 def test_from_blocks_contract():

@@ -93,16 +93,23 @@ def test_method_names():
         bse.method_from_name("qr")
 
 
-def test_negative_spectrum_host():
+def test_negative_spectrum_shape_check_host():
+    """solvers.cpp:225-228: the shape check runs on the host before any device work."""
     lam = np.array([1.0, 2.0])
     v = np.arange(8, dtype=complex).reshape(4, 2)
     h = bse.BseMatrixI(np.eye(2, dtype=complex), np.zeros((2, 2), complex))
-    neg = bse.negative_spectrum(h, bse.SpectralResult(lam, v, bse.Method.Chol, [1]))
-    assert np.array_equal(neg.lambda_, -lam)
-    assert np.array_equal(neg.v[:2], v[2:]) and np.array_equal(neg.v[2:], v[:2])
-    assert neg.near_singular == [1]
     with pytest.raises(bse.DimensionMismatch):
         bse.negative_spectrum(h, bse.SpectralResult(lam, v[:3], bse.Method.Chol))
+
+
+def test_check_pairing_and_error_model_host():
+    """verify.cpp:95-114 are host formulas (sorting / scalars)."""
+    assert bse.check_pairing([1.0, 3.0, 2.0], [-2.0, -1.0, -3.0], 0.0)
+    assert not bse.check_pairing([1.0, 3.0], [-1.0, -3.1], 1e-3)
+    with pytest.raises(bse.LengthMismatch):
+        bse.check_pairing([1.0], [-1.0, -2.0], 1e-3)
+    e = bse.machine_eps()
+    assert bse.predicted_error(4.0, 1.0) == e * 4.0
 
 
 def _mt19937_64(seed):
