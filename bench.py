@@ -298,6 +298,11 @@ def main():
             # ncu dram bytes / algorithmic bytes of one captured launch, applied per launch
             roofline["traffic"] = tr["ratio"] * roofline["algorithmic_bytes_per_launch"]
             roofline["traffic_source"] = tr.get("capture")
+        if roofline["bound"] == "tensor" and "bytes_per_flop" in tr:
+            # ncu dram bytes per executed flop of the captured 4096^3 launch, per average launch
+            roofline["traffic"] = tr["bytes_per_flop"] * gemm["flops"] / max(gemm["launches"], 1)
+            roofline["traffic_unit"] = "bytes per launch (DRAM read + write)"
+            roofline["traffic_source"] = tr.get("capture")
     except Exception:
         pass
 

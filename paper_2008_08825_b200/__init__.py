@@ -35,6 +35,7 @@ __all__ = [
     "solve", "negative_spectrum", "hermitian_eig", "cholesky_lower", "svd", "tri_solve", "matmul",
     "solve_sqrt", "solve_reference", "hpd_sqrt", "residual", "sigma_orthogonality_error",
     "check_form1", "check_form2", "check_pairing", "predicted_error", "OddDimension",
+    "residual_device", "sigma_orthogonality_error_device",
     "LengthMismatch",
     "Context", "default_context", "method_name", "method_from_name", "machine_eps",
     "K_DEFAULT_HERM_TOL",
@@ -429,6 +430,33 @@ def residual(h: BseMatrixI, r: SpectralResult, ctx: Optional[Context] = None) ->
     _check(_lib.lib().bse_residual(ctx.handle, n, _p(h.a), n, _p(h.b), n, k, _p(lam), _p(v),
                                    2 * n, _p(out), ctypes.byref(st)), st)
     return out
+
+
+def residual_device(n: int, a_ptr: int, b_ptr: int, k: int, lam_ptr: int, v_ptr: int,
+                    out_ptr: int, ctx: Optional[Context] = None, lda: Optional[int] = None,
+                    ldb: Optional[int] = None, ldv: Optional[int] = None) -> None:
+    """bse_residual_device: device pointers (e.g. torch data_ptr()); out is k doubles."""
+    ctx = ctx or default_context()
+    st = Status()
+    _check(_lib.lib().bse_residual_device(ctx.handle, n, ctypes.c_void_p(a_ptr), lda or n,
+                                          ctypes.c_void_p(b_ptr), ldb or n, k,
+                                          ctypes.c_void_p(lam_ptr), ctypes.c_void_p(v_ptr),
+                                          ldv or 2 * n, ctypes.c_void_p(out_ptr),
+                                          ctypes.byref(st)), st)
+
+
+def sigma_orthogonality_error_device(rows: int, k: int, v_ptr: int,
+                                     ctx: Optional[Context] = None,
+                                     ldv: Optional[int] = None) -> float:
+    """bse_sigma_orthogonality_error_device: V on the device, scalar result on the host."""
+    ctx = ctx or default_context()
+    out = ctypes.c_double(0.0)
+    st = Status()
+    _check(_lib.lib().bse_sigma_orthogonality_error_device(ctx.handle, rows, k,
+                                                           ctypes.c_void_p(v_ptr), ldv or rows,
+                                                           ctypes.byref(out), ctypes.byref(st)),
+           st)
+    return out.value
 
 
 def sigma_orthogonality_error(v, ctx: Optional[Context] = None) -> float:

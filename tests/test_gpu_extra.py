@@ -227,3 +227,23 @@ def test_predicted_error_formula():
     e = bse.machine_eps()
     assert bse.predicted_error(10.0, 0.5, 0.5) == e * 10.0 / 0.5
     assert bse.predicted_error(10.0, 0.5, 0.5, squared_method=True) == e * 20.0 * min(20.0, 1 / np.sqrt(e))
+
+
+def test_device_diagnostics_through_torch_buffers():
+    """bse_residual_device / bse_sigma_orthogonality_error_device on device-resident data
+    (the at-scale validation path of tools/big_check.py), against the host-pointer versions."""
+    torch = pytest.importorskip("torch")
+    a, b = configs.config2(13, n=300)
+    h = bse.from_blocks(a, b)
+    r = bse.solve_chol(h)
+    dev = torch.device("cuda", 0)
+    da = torch.from_numpy(np.ascontiguousarray(h.a.T)).to(dev)
+    db = torch.from_numpy(np.ascontiguousarray(h.b.T)).to(dev)
+    dv = torch.from_numpy(np.ascontiguousarray(r.v.T)).to(dev)
+    dl = torch.from_numpy(r.lambda_.copy()).to(dev)
+    out = torch.empty(300, dtype=torch.float64, device=dev)
+    bse.residual_device(300, da.data_ptr(), db.data_ptr(), 300, dl.data_ptr(), dv.data_ptr(),
+                        out.data_ptr())
+    assert np.array_equal(out.cpu().numpy(), bse.residual(h, r))  # deterministic, same kernels
+    s = bse.sigma_orthogonality_error_device(600, 300, dv.data_ptr())
+    assert s == bse.sigma_orthogonality_error(r.v)
