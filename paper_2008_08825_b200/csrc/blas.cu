@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(256) ztrtri_diag_kernel(int64_t n, const z_t* 
     if (col < jb && i > col) {
       for (int kk = col + q; kk < i; kk += 4) zfma(part, Ls[i + kk * (nb + 1)], Xs[kk * (nb + 1) + col]);
     }
+    warp_converge();
     part.x += __shfl_xor_sync(0xffffffffu, part.x, 1);
     part.y += __shfl_xor_sync(0xffffffffu, part.y, 1);
     part.x += __shfl_xor_sync(0xffffffffu, part.x, 2);

@@ -97,17 +97,29 @@ __device__ __forceinline__ void zcfma(z_t& acc, z_t a, z_t b) {
 __device__ __forceinline__ double zabs2(z_t a) { return a.x * a.x + a.y * a.y; }
 
 // ------------------------------------------------------------------ warp/block reductions
+// Every warp-collective helper starts with warp_converge(): a warp that reaches a full-mask
+// shuffle in a diverged state (after lane-dependent branches) otherwise takes the BRA.DIV
+// fallback path, measured at ~14k cycles for a handful of shuffles in the panel kernels.
+// (A plain __syncwarp() is folded away by the compiler there; the volatile bar.warp.sync
+// stays.)
+__device__ __forceinline__ void warp_converge() { asm volatile("bar.warp.sync -1;" ::: "memory"); }
 __device__ __forceinline__ double warp_sum(double v) {
+  warp_converge();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 __device__ __forceinline__ z_t warp_zsum(z_t v) {
-  v.x = warp_sum(v.x);
-  v.y = warp_sum(v.y);
+  warp_converge();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
   return v;
 }
 __device__ __forceinline__ double warp_max(double v) {
+  warp_converge();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
@@ -170,6 +182,7 @@ __device__ __forceinline__ z_t zsum_strided16(const z_t* p, int64_t es, int star
 // complex shuffles in all); on return lane l holds the total of value (l >> 1).
 __device__ __forceinline__ z_t warp_transpose_zsum16(z_t (&v)[16]) {
   const int lane = threadIdx.x & 31;
+  warp_converge();
 #pragma unroll
   for (int st = 0; st < 4; ++st) {
     const int h = 8 >> st, o = 16 >> st;
@@ -187,15 +200,43 @@ __device__ __forceinline__ z_t warp_transpose_zsum16(z_t (&v)[16]) {
     }
   }
   z_t r;
+  warp_converge();
   r.x = __shfl_xor_sync(0xffffffffu, v[0].x, 1);
   r.y = __shfl_xor_sync(0xffffffffu, v[0].y, 1);
   return zadd(v[0], r);
+}
+
+// Sums each of 16 complex values over the 8 lanes of a warp that share lane bits 0..1 (the
+// rows of a 4-lanes-per-row mapping), by halving over lane bits 4, 3, 2. On return a lane
+// holds the totals of values idx and idx + 1, idx = 8 b4 + 4 b3 + 2 b2.
+__device__ __forceinline__ void warp_transpose_zsum16_rows(z_t (&v)[16], z_t& t0, z_t& t1) {
+  const int lane = threadIdx.x & 31;
+  warp_converge();
+#pragma unroll
+  for (int st = 0; st < 3; ++st) {
+    const int h = 8 >> st, o = 16 >> st;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < h) {
+        const z_t keep = up ? v[h + j] : v[j];
+        const z_t send = up ? v[j] : v[h + j];
+        z_t r;
+        r.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+        r.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+        v[j] = zadd(keep, r);
+      }
+    }
+  }
+  t0 = v[0];
+  t1 = v[1];
 }
 
 // Sums each of 8 complex values over the 32 lanes of a warp (9 complex shuffles in all); on
 // return lanes 4j..4j+3 hold the total of value j.
 __device__ __forceinline__ z_t warp_transpose_zsum8(z_t (&v)[8]) {
   const int lane = threadIdx.x & 31;
+  warp_converge();
 #pragma unroll
   for (int st = 0; st < 3; ++st) {
     const int h = 4 >> st, o = 16 >> st;
@@ -213,6 +254,7 @@ __device__ __forceinline__ z_t warp_transpose_zsum8(z_t (&v)[8]) {
     }
   }
   z_t t = v[0];
+  warp_converge();
 #pragma unroll
   for (int o = 2; o >= 1; o >>= 1) {
     t.x += __shfl_xor_sync(0xffffffffu, t.x, o);

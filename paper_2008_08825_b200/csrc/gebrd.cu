@@ -109,6 +109,7 @@ __device__ __forceinline__ void gb_tsum(const z_t* partial, int stride, int off,
   const int kk = threadIdx.x >> 2, part = threadIdx.x & 3;
   z_t s = make_double2(0.0, 0.0);
   if (kk < nsum && kk < pmax) s = zsum_strided16(partial + off + kk, stride, c_lo + part, c_hi, 4);
+  warp_converge();
   s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
   s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
   s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);

@@ -138,8 +138,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   z_t* vbuf = reinterpret_cast<z_t*>(bars + 2 * kRing);  // 2 x [v rows | v cols] of a tile
   int* ttab = reinterpret_cast<int*>(vbuf + 4 * kT);       // this CTA's tiles: bi | bj << 16
   z_t* swp = reinterpret_cast<z_t*>(ttab + kTabMax);       // 2 x (8 x kT + kT): sweep partials
-  z_t* red = swp;                          // kQ x kT reduction scratch (phase B; aliases swp)
-  z_t* red2 = red + kQ * kT;               // kQ x kT reduction scratch
   z_t* wg = swp + 2 * (8 * kT + kT);       // NB : W(g+1, p)
   z_t* vg = wg + NB;                       // NB : V(g+1, p)
   z_t* xs = vg + NB;                       // kT : next column values of the slab
@@ -334,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int p = kk & (NB - 1);
       z_t s = zero;
       if (p < i) s = zsum_strided16(a.s12p + kk, 2 * NB, int(g / kT) + part, a.nch, 4);
+      warp_converge();
       s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
       s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
       s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
@@ -351,54 +350,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     grid.sync();
     trace(i, 3);
     // ---------------------------------------------------------------- phase B
+    // Mapping: 4 consecutive lanes (sq = lane & 3) share a slab row (srl = tid >> 2) and split
+    // the panel columns p = sq + 4k. Cross-lane sums are shuffles, the column sums over the
+    // slab rows are warp transpose-reductions plus one shared-memory exchange: two CTA
+    // barriers per slab (one more on the first slab for the broadcast scalars).
     const int c0 = int(g1 / kT);
-    double alw = 0.0;  // alpha of W (register: block_sum below reuses dred)
+    const int srl = tid >> 2, sq = tid & 3;
+    double alw = 0.0;  // alpha of W
+    z_t* part = swp;   // [8 warps][4 sq][16] column-sum partials of the slab
+    double* nrmw = reinterpret_cast<double*>(swp + 8 * 4 * 16);  // [8] row-norm partials
     for (int c = first_owned(c0, cta, G), first = 1; c < a.nch; c += G, first = 0) {
-      const int64_t r = int64_t(c) * kT + rl;
+      const int64_t r = int64_t(c) * kT + srl;
       const bool valid = r < n && r >= g1;
       // every load of the phase is issued before the first consumer
       z_t vrr[NB / kQ], wrr[NB / kQ], vri = zero, xold = zero, ypart = zero;
-      // warp 0 (first slab): raw terms of v^H A v (G <= 256 per-CTA partials) and of
-      // y(g+1) (chunk partials c0 + lane + 32u), summed after the barrier
       double vavr[8];
-      z_t ysr[8], vgp = zero, wgp = zero, tpre = zero;
+      z_t ysr[8], vgp = zero, wgp = zero, tq0 = zero, tq1 = zero;
       const z_t* yrow = a.Y + int64_t(c0) * a.nch * kT + (g1 % kT);
-      if (first) {
-        if (warp == 0) {
+      if (first && warp == 0) {  // per-column scalars, summed by warp 0 after the loads
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            vavr[u] = (lane + 32 * u < G) ? a.vav[lane + 32 * u] : 0.0;
-            const int m = c0 + lane + 32 * u;
-            ysr[u] = (m < a.nch) ? yrow[int64_t(m) * kT] : zero;
-          }
-          if (lane < i) {
-            vgp = V[g1 + int64_t(lane) * ldp];
-            wgp = W[g1 + int64_t(lane) * ldp];
-          }
+        for (int u = 0; u < 8; ++u) {
+          vavr[u] = (lane + 32 * u < G) ? a.vav[lane + 32 * u] : 0.0;
+          const int m = c0 + lane + 32 * u;
+          ysr[u] = (m < a.nch) ? yrow[int64_t(m) * kT] : zero;
         }
-        if (tid >= 64 && tid < 64 + 2 * NB) tpre = a.t12[tid - 64];  // zero beyond i
+        if (lane < i) {
+          vgp = V[g1 + int64_t(lane) * ldp];
+          wgp = W[g1 + int64_t(lane) * ldp];
+        }
+        tq0 = a.t12[lane];       // t1 (zero beyond i)
+        tq1 = a.t12[NB + lane];  // t2
       }
 #pragma unroll
       for (int k = 0; k < NB / kQ; ++k) {
-        const int p = q + k * kQ;
+        const int p = sq + k * kQ;
         vrr[k] = (valid && p < i) ? V[r + int64_t(p) * ldp] : zero;
         wrr[k] = (valid && p < i) ? W[r + int64_t(p) * ldp] : zero;
       }
       if (valid) {
         vri = V[r + int64_t(i) * ldp];
-        if (has_next && q == 0) xold = a.A[r + g1 * lda];
-        ypart = zsum_strided16(a.Y + int64_t(c) * a.nch * kT + rl, kT, c0 + q, a.nch, kQ);
+        if (has_next) xold = a.A[r + g1 * lda];
+        ypart = zsum_strided16(a.Y + int64_t(c) * a.nch * kT + srl, kT, c0 + sq, a.nch, kQ);
       }
       if (first) {
-        if (tid >= 64 && tid < 64 + 2 * NB) tt[tid - 64] = tpre;
+        // A CTA barrier (WARPSYNC.ALL + BAR) re-converges warp 0 before its butterflies:
+        // after the lane-dependent load loops above the hardware may still see the warp as
+        // diverged, and full-mask shuffles then take the WARPSYNC.COLLECTIVE fallback
+        // (measured: 14k cycles for this block instead of ~600).
         __syncthreads();
         if (warp == 0) {  // row g+1 of V and W; alpha of W (same fixed order in every CTA)
-          z_t corr = zero;
-          double vt = 0.0;
-          if (lane < i) {
-            corr = zadd(zmul(vgp, tt[lane]), zmul(wgp, tt[NB + lane]));
-            vt = zcmul(tt[NB + lane], tt[lane]).x;
-          }
+          tt[lane] = tq0;
+          tt[NB + lane] = tq1;
+          // branch-free up to the shuffles (lane-dependent branches leave the warp diverged at
+          // the butterflies, which then take the slow BRA.DIV path)
+          const bool act = lane < i;
+          const z_t cp = zadd(zmul(vgp, tq0), zmul(wgp, tq1));
+          z_t corr = act ? cp : zero;
+          double vt = act ? zcmul(tq1, tq0).x : 0.0;
           double vs = 0.0;
           z_t ysum = zero;
 #pragma unroll
@@ -406,22 +414,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             vs += vavr[u];
             ysum = zadd(ysum, ysr[u]);
           }
-          for (int m = c0 + lane + 256; m < a.nch; m += 32) ysum = zadd(ysum, yrow[int64_t(m) * kT]);
+          for (int mm = 256; c0 + mm < a.nch; mm += 32) {  // warp-uniform trip count (n > 16384)
+            const int m = c0 + mm + lane;
+            if (m < a.nch) ysum = zadd(ysum, yrow[int64_t(m) * kT]);
+          }
           const double vw0 = warp_sum(vs);
           const z_t y = warp_zsum(ysum);
           corr = warp_zsum(corr);
           // v^H w' = v^H A v - sum_p [conj(t2_p) t1_p + conj(t1_p) t2_p]  (real)
           const double vw = vw0 - 2.0 * warp_sum(vt);
           const double alw0 = -0.5 * zabs2(tau) * vw;  // alpha of W = tau w' + alpha v (real)
+          // y, corr, vw are butterfly sums: identical in every lane, so lane i forms W(g+1, i)
+          // itself (no second writer of wg[i])
+          const z_t tw = zmul(tau, zsub(y, corr));
           if (lane < NB) {
             vg[lane] = lane < i ? vgp : (lane == i ? one : zero);
-            wg[lane] = lane < i ? wgp : zero;
+            wg[lane] = lane < i ? wgp : (lane == i ? make_double2(tw.x + alw0, tw.y) : zero);
           }
-          if (lane == 0) {
-            const z_t tw = zmul(tau, zsub(y, corr));
-            wg[i] = make_double2(tw.x + alw0, tw.y);
-            dred[1] = alw0;
-          }
+          if (lane == 0) dred[1] = alw0;
         }
         __syncthreads();
         alw = dred[1];
@@ -430,71 +440,80 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (valid) {
 #pragma unroll
         for (int k = 0; k < NB / kQ; ++k) {
-          const int p = q + k * kQ;
+          const int p = sq + k * kQ;
           if (p < i) {
             ypart = zsub(ypart, zadd(zmul(vrr[k], tt[p]), zmul(wrr[k], tt[NB + p])));
             upd = zadd(upd, zadd(zmul(vrr[k], zconj(wg[p])), zmul(wrr[k], zconj(vg[p]))));
           }
         }
       }
-      red[q * kT + rl] = ypart;
-      red2[q * kT + rl] = upd;
+      // the 4 lanes of a row get bit-identical sums ((a+b)+(c+d) in every lane); the CTA
+      // barrier re-converges the warps before the shuffles (see the first-slab block)
       __syncthreads();
-      z_t xn = zero;
-      if (q == 0) {
-        z_t wri = zero;
-        if (valid) {
-          z_t y = red[rl], u = red2[rl];
 #pragma unroll
-          for (int qq = 1; qq < kQ; ++qq) {
-            y = zadd(y, red[qq * kT + rl]);
-            u = zadd(u, red2[qq * kT + rl]);
-          }
-          wri = zadd(zmul(tau, y), zscale(vri, alw));
-          if (r == g1) wri = wg[i];  // the value every CTA used for row g+1
+      for (int o = 1; o <= 2; o <<= 1) {
+        ypart.x += __shfl_xor_sync(0xffffffffu, ypart.x, o);
+        ypart.y += __shfl_xor_sync(0xffffffffu, ypart.y, o);
+        upd.x += __shfl_xor_sync(0xffffffffu, upd.x, o);
+        upd.y += __shfl_xor_sync(0xffffffffu, upd.y, o);
+      }
+      z_t xn = zero, wri = zero;
+      if (valid) {
+        wri = zadd(zmul(tau, ypart), zscale(vri, alw));
+        if (r == g1) wri = wg[i];  // the value every CTA used for row g+1
+        z_t x = zero;
+        if (has_next) {
+          // a(r, g+1) -= sum_{p<=i} V(r,p) conj(W(g+1,p)) + W(r,p) conj(V(g+1,p))
+          x = zsub(xold, upd);
+          x = zsub(x, zadd(zmul(vri, zconj(wg[i])), wri));  // p = i, V(g+1,i) = 1
+          if (r == g1) x.y = 0.0;
+          if (r >= g1 + 2) xn = x;
+        }
+        if (sq == 0) {
           W[r + int64_t(i) * ldp] = wri;
           a.WV[r + int64_t(i) * ldp] = wri;
           if (r >= g1 + 1) a.A[r + g * lda] = vri;  // reflector storage below the subdiagonal
           if (has_next) {
-            // a(r, g+1) -= sum_{p<=i} V(r,p) conj(W(g+1,p)) + W(r,p) conj(V(g+1,p))
-            z_t x = zsub(xold, u);
-            x = zsub(x, zadd(zmul(vri, zconj(wg[i])), wri));  // p = i, V(g+1,i) = 1
-            if (r == g1) {
-              x.y = 0.0;
-              a.d[g1] = x.x;
-            }
+            if (r == g1) a.d[g1] = x.x;
             a.A[r + g1 * lda] = x;
-            if (r >= g1 + 2) xn = x;
           }
         }
-        xs[rl] = xn;
-        wc[rl] = wri;
       }
       if (has_next) {
-        const double nrm = block_sum(q == 0 ? zabs2(xn) : 0.0, dred);  // syncs: xs, wc visible
-        if (tid == 0) a.normp[c] = nrm;
-        // s1[p] = sum conj(W(r,p)) x(r), s2[p] = sum conj(V(r,p)) x(r), p <= i, over the slab,
-        // from the rows held in registers
-        const z_t xv = xs[rl], wci = wc[rl];
+        // s1[p] = sum conj(W(r,p)) x(r), s2[p] = sum conj(V(r,p)) x(r), p <= i, and ||x||^2
         z_t pr[16];
 #pragma unroll
         for (int k = 0; k < NB / kQ; ++k) {
-          const int p = q + k * kQ;
+          const int p = sq + k * kQ;
           pr[k] = zero;
           pr[8 + k] = zero;
-          zcfma(pr[k], (p == i) ? wci : wrr[k], xv);
-          zcfma(pr[8 + k], (p == i) ? vri : vrr[k], xv);
+          zcfma(pr[k], (p == i) ? wri : wrr[k], xn);
+          zcfma(pr[8 + k], (p == i) ? vri : vrr[k], xn);
         }
-        const z_t tot = warp_transpose_zsum16(pr);
-        const int idx = lane >> 1;
-        if ((warp & 1) && !(lane & 1)) red[q * 16 + idx] = tot;  // rows 32..63 of the slab
+        z_t t0, t1;
+        __syncthreads();  // re-converge after the lane-dependent stores above
+        warp_transpose_zsum16_rows(pr, t0, t1);  // over the warp's 8 rows (lane bits 2..4)
+        const int idx = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1);
+        part[(warp * 4 + sq) * 16 + idx] = t0;
+        part[(warp * 4 + sq) * 16 + idx + 1] = t1;
+        const double nr = warp_sum(sq == 0 ? zabs2(xn) : 0.0);
+        if (lane == 0) nrmw[warp] = nr;
         __syncthreads();
-        if (!(warp & 1) && !(lane & 1)) {
-          const int p = q + (idx & 7) * kQ;
-          if (p <= i) a.s12p[int64_t(c) * 2 * NB + (idx >> 3) * NB + p] = zadd(tot, red[q * 16 + idx]);
+        if (tid < 64) {  // (sq, idx) = (tid >> 4, tid & 15): fixed-order sum over the 8 warps
+          const int q2 = tid >> 4, id = tid & 15;
+          z_t sum = part[q2 * 16 + id];
+#pragma unroll
+          for (int w = 1; w < 8; ++w) sum = zadd(sum, part[(w * 4 + q2) * 16 + id]);
+          const int p = q2 + (id & 7) * kQ;
+          if (p <= i) a.s12p[int64_t(c) * 2 * NB + (id >> 3) * NB + p] = sum;
+        } else if (tid == 64) {
+          double nsum = nrmw[0];
+#pragma unroll
+          for (int w = 1; w < 8; ++w) nsum += nrmw[w];
+          a.normp[c] = nsum;
         }
+        if (c + G < a.nch) __syncthreads();  // part / nrmw are reused by the next slab
       }
-      __syncthreads();
     }
     trace(i, 4);
     if (has_next) grid.sync();

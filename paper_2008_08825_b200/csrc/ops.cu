@@ -288,6 +288,7 @@ __global__ void tgk_refine_kernel(int64_t n, const double* __restrict__ a2, doub
     int c = 0;
     if (lane == 0) c = tgk_count_below(n, a2, lo, pivmin) - int(n);
     else if (lane == 1) c = tgk_count_below(n, a2, hi, pivmin) - int(n);
+    warp_converge();
     const int clo = __shfl_sync(0xffffffffu, c, 0), chi = __shfl_sync(0xffffffffu, c, 1);
     if (!(clo <= i && chi >= i + 1)) {
       lo = 0.0;

@@ -582,6 +582,7 @@ __global__ void __launch_bounds__(256) stedc_zhat_kernel(StedcLevel lv) {
       prod *= (j == i) ? dij : dij / (dl[i] - dl[j]);
     }
 #pragma unroll
+    warp_converge();
     for (int o = 16; o > 0; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
     if (lane == 0) {
       const double v = sqrt(fabs(prod));
