@@ -36,7 +36,34 @@ void launch_z(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   BSE_LAUNCH_CHECK();
 }
 
+// Short-K variant (k <= 128: the panel trailing updates, HERK steps, back-transform
+// applications): 8 warps of 32x16 per 64x64 tile (half the accumulators per thread), so
+// twice the warps per SM hide each tile's prologue and C round trips.
+constexpr int kSTs = 4, kMinBs = 2, kWNs = 16;  // 8 warps of 32x16 per 64x64 tile
+
+template <bool CA, bool CB>
+void launch_z_short(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
+  using T = ZGemmTile<kBM, kBN, kBK, kWM, kWNs, kSTs, CA, CB>;
+  auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWNs, kSTs, CA, CB, kMinBs>;
+  static bool configured = false;
+  if (!configured) {
+    BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(T::SMEM)));
+    configured = true;
+  }
+  kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
+  BSE_LAUNCH_CHECK();
+}
+
 void launch_z_any(cudaStream_t s, int opa, int opb, const ZGemmParams& p, dim3 grid) {
+  static const bool no_short = getenv("BSE_GEMM_NO_SHORT") != nullptr;  // A/B switch
+  if (p.k <= 128 && p.ksplit == 1 && !no_short) {
+    if (!opa && !opb) launch_z_short<false, false>(s, p, grid);
+    else if (!opa && opb) launch_z_short<false, true>(s, p, grid);
+    else if (opa && !opb) launch_z_short<true, false>(s, p, grid);
+    else launch_z_short<true, true>(s, p, grid);
+    return;
+  }
   if (!opa && !opb) launch_z<false, false>(s, p, grid);
   else if (!opa && opb) launch_z<false, true>(s, p, grid);
   else if (opa && !opb) launch_z<true, false>(s, p, grid);

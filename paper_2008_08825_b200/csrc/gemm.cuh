@@ -75,8 +75,10 @@ struct ZGemmTile {
   static_assert((BM * BK) % NTHREADS == 0 && (BN * BK) % NTHREADS == 0, "loader");
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool CONJ_A, bool CONJ_B>
-__global__ void __launch_bounds__(ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, CONJ_B>::NTHREADS)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool CONJ_A, bool CONJ_B,
+          int MINB = 1>
+__global__ void __launch_bounds__(ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, CONJ_B>::NTHREADS,
+                                  MINB)
     zgemm_dmma_kernel(ZGemmParams p) {
   using T = ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, CONJ_B>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -213,11 +215,12 @@ __global__ void __launch_bounds__(ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, 
   // later reads, so the compiler cannot hoist loads over them): 2 memory round trips per tile
   // instead of one per element, which dominates short-K products (k = 64 trailing updates).
   const bool use_beta = p.ksplit == 1 && (p.beta.x != 0.0 || p.beta.y != 0.0);
+  constexpr int ER = 2;  // fragment rows per C read round
 #pragma unroll
-  for (int a0 = 0; a0 < T::MT; a0 += 2) {
-    z_t cv[2][T::NT][2];
+  for (int a0 = 0; a0 < T::MT; a0 += ER) {
+    z_t cv[ER][T::NT][2];
 #pragma unroll
-    for (int da = 0; da < 2; ++da)
+    for (int da = 0; da < ER; ++da)
 #pragma unroll
       for (int b = 0; b < T::NT; ++b)
 #pragma unroll
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, 
           cv[da][b][h] = live ? C[gi + gj * p.ldc] : make_double2(0.0, 0.0);
         }
 #pragma unroll
-    for (int da = 0; da < 2; ++da)
+    for (int da = 0; da < ER; ++da)
 #pragma unroll
       for (int b = 0; b < T::NT; ++b)
 #pragma unroll
