@@ -533,7 +533,7 @@ int bse_svd(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* u, int6
     h2d(c, dM, n, m, ldm, n, n);
     zgebrd_upper(sm, n, dM, n, d, e, tq, tp, ws_gb);
     tgk_build(sm, n, d, e, td, te);
-    dstedc(sm, m2, td, te, X, ws_st, info);
+    dstedc(sm, m2, td, te, X, ws_st, info, n);  // only the positive half of the vectors
     tgk_extract(sm, n, X, dU, n, dV, n);
     zunmbr_q(sm, n, dM, n, tq, dU, n, n, ws_um);
     zunmbr_p(sm, n, dM, n, tp, dV, n, n, ws_um);

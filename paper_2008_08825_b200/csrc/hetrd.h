@@ -27,6 +27,7 @@ void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z
 // Q (n x n, ld n, real) the orthonormal eigenvectors. Returns nonzero on failure.
 size_t stedc_workspace_bytes(int64_t n);
 void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, void* ws,
-            int* d_info);
+            int* d_info,
+            int64_t keep_from = 0);
 
 }  // namespace bseg

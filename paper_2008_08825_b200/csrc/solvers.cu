@@ -224,7 +224,7 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   zgebrd_upper(s, n, b2, ld, d, e, tauq, taup, ws_gebrd);
   clk.mark();
   tgk_build(s, n, d, e, td, te);
-  dstedc(s, m2, td, te, X, ws_stedc, info + 2);
+  dstedc(s, m2, td, te, X, ws_stedc, info + 2, n);  // only the positive half of the vectors
   clk.mark();
   // ascending singular values = top n TGK eigenvalues; vectors u (b3), v (b4)
   BSE_CUDA(cudaMemcpyAsync(sasc, td + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));

@@ -77,6 +77,7 @@ struct StedcLevel {
   double* UT;       // (k1+k2) x K, ld n, column block at s
   double* UB;       // (k2+k3) x K
   int* info;
+  int64_t keep_from;  // > 0 on the last level: output columns below it are not needed
 };
 
 // ----------------------------------------------------------------------------- setup
@@ -672,6 +673,18 @@ __global__ void __launch_bounds__(GT::NTHREADS) stedc_gemm_kernel(StedcLevel lv,
   const int tm = local % tiles_m, tn = local / tiles_m;
   const int64_t m0 = int64_t(tm) * gBM, n0 = int64_t(tn) * gBN;
   if (n0 >= ncols) return;
+  // Wanted columns only (e.g. the positive half of the TGK spectrum): roots are ascending and
+  // their merged positions monotone, so the unwanted roots are a prefix j < jlo.
+  int jlo = 0;
+  if (lv.keep_from > s) {
+    int lo2 = 0, hi2 = ncols;  // first j with s + pos[s + j] >= keep_from
+    while (lo2 < hi2) {
+      const int m = (lo2 + hi2) >> 1;
+      if (s + lv.pos[s + m] >= lv.keep_from) hi2 = m; else lo2 = m + 1;
+    }
+    jlo = lo2;
+    if (n0 + gBN <= jlo) return;
+  }
   const double* A = lv.Qold + (s + (half ? md.n1 : 0));
   const int* acol = half ? (lv.acolB + s) : (lv.acolT + s);
   const double* B = (half ? lv.UB : lv.UT) + int64_t(s) * n;  // ld n
@@ -745,7 +758,7 @@ __global__ void __launch_bounds__(GT::NTHREADS) stedc_gemm_kernel(StedcLevel lv,
       for (int h = 0; h < 2; ++h) {
         const int64_t gi = m0 + wm0 + a * 8 + fr;
         const int64_t gj = n0 + wn0 + b * 8 + 2 * fk + h;
-        if (gi >= rows || gj >= ncols) continue;
+        if (gi >= rows || gj >= ncols || gj < jlo) continue;
         C[gi + int64_t(ccol[gj]) * n] = acc[a][b][h];
       }
 }
@@ -802,7 +815,7 @@ T* carve(char*& p, size_t count) {
 }  // namespace
 
 void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, void* ws,
-            int* d_info) {
+            int* d_info, int64_t keep_from) {
   BSE_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), s));
   if (n <= 0) return;
   char* p = reinterpret_cast<char*>(ws);
@@ -888,6 +901,7 @@ void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, vo
     lv.defcol = defcol; lv.orig = orig; lv.tau = tau; lv.what = what; lv.pos = pos;
     lv.defpos = defpos; lv.rowT = rowT; lv.rowB = rowB; lv.acolT = acolT; lv.acolB = acolB;
     lv.ccol = ccol; lv.UT = UT; lv.UB = UB; lv.info = d_info;
+    lv.keep_from = (lvl == 0) ? keep_from : 0;
     {
       const int64_t half = int64_t(maxN / 2 + 1) * (maxN / 2 + 1) * 2;
       const unsigned gx = unsigned(std::min<int64_t>(ceil_div(half, 256), 4096 / std::max(1, nm) + 1));
