@@ -267,16 +267,20 @@ __global__ void __launch_bounds__(256) stedc_prepare_kernel(StedcLevel lv) {
     zs[rank] = zv * rinv2;
   }
   __shared__ int sh_npairs, sh_K, sh_ndef;
-  __shared__ double sh_rho;
+  __shared__ double sh_rho, sh_max[32];
+  __syncthreads();
+  {  // max(|D|, |z|) over the merge: block-parallel (max is order independent)
+    double mx = 0.0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) mx = fmax(mx, fmax(fabs(ds[j]), fabs(zs[j])));
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) sh_max[threadIdx.x >> 5] = mx;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     const double rho = 2.0 * fabs(beta);
-    double dmax = 0.0, zmax = 0.0;
-    for (int j = 0; j < N; ++j) {
-      dmax = fmax(dmax, fabs(ds[j]));
-      zmax = fmax(zmax, fabs(zs[j]));
-    }
-    const double tol = 8.0 * kEps * fmax(dmax, zmax);
+    double dzmax = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) dzmax = fmax(dzmax, sh_max[w]);
+    const double tol = 8.0 * kEps * dzmax;
     int K = 0, ndef = 0, npairs = 0;
     double* dl = lv.dl + s;
     double* w = lv.w + s;
@@ -304,21 +308,33 @@ __global__ void __launch_bounds__(256) stedc_prepare_kernel(StedcLevel lv) {
     };
     int pj = -1, tpj = 0;
     double dpj = 0.0, zpj = 0.0;
-    for (int j = 0; j < N; ++j) {
-      const int nj = perm[j];
-      const double dnj = ds[j];
-      const double znj = zs[j];
+    // The scan is inherently sequential; its inputs are streamed through registers in
+    // chunks of kCh (fully unrolled, so no local memory), the next chunk's loads issued before
+    // the current chunk is processed.
+    constexpr int kCh = 8;
+    auto step = [&](int nj, double dnj, double znj) {
       const int tnj = nj < n1 ? 1 : 3;
       if (rho * fabs(znj) <= tol) {
         push_def(dnj, nj);
-        continue;
+        return;
       }
       if (pj < 0) {
         pj = nj; dpj = dnj; zpj = znj; tpj = tnj;
-        continue;
+        return;
+      }
+      const double t = dnj - dpj;
+      // dlaed2's close-pair test |t c s| <= tol with c = z_j / tau, s = -z_p / tau equals
+      // |t z_j z_p| <= tol (z_j^2 + z_p^2); that cheap form (no hypot / divisions on the
+      // sequential path) screens out the pairs that are clearly not deflated, the exact
+      // LAPACK arithmetic decides the rest.
+      const double zz = znj * znj + zpj * zpj;
+      if (fabs(t * znj * zpj) > 2.0 * tol * zz) {
+        dl[K] = dpj; w[K] = zpj; ndcol[K] = pj; ndtype[K] = tpj;
+        ++K;
+        pj = nj; dpj = dnj; zpj = znj; tpj = tnj;
+        return;
       }
       const double tau = hypot(znj, zpj);
-      const double t = dnj - dpj;
       const double cv = znj / tau, sv = -zpj / tau;
       if (fabs(t * cv * sv) <= tol) {
         rot_a[npairs] = pj;
@@ -335,6 +351,32 @@ __global__ void __launch_bounds__(256) stedc_prepare_kernel(StedcLevel lv) {
         dl[K] = dpj; w[K] = zpj; ndcol[K] = pj; ndtype[K] = tpj;
         ++K;
         pj = nj; dpj = dnj; zpj = znj; tpj = tnj;
+      }
+    };
+    int cn[kCh], xn[kCh];
+    double cd[kCh], cz[kCh], xd[kCh], xz[kCh];
+#pragma unroll
+    for (int u = 0; u < kCh; ++u) {
+      cn[u] = u < N ? perm[u] : 0;
+      cd[u] = u < N ? ds[u] : 0.0;
+      cz[u] = u < N ? zs[u] : 0.0;
+    }
+    for (int j0 = 0; j0 < N; j0 += kCh) {
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {  // next chunk in flight
+        const int jj = j0 + kCh + u;
+        xn[u] = jj < N ? perm[jj] : 0;
+        xd[u] = jj < N ? ds[jj] : 0.0;
+        xz[u] = jj < N ? zs[jj] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCh; ++u)
+        if (j0 + u < N) step(cn[u], cd[u], cz[u]);
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        cn[u] = xn[u];
+        cd[u] = xd[u];
+        cz[u] = xz[u];
       }
     }
     if (pj >= 0) {
@@ -582,8 +624,8 @@ __global__ void __launch_bounds__(256) stedc_zhat_kernel(StedcLevel lv) {
       const double dij = (dl[i] - dl[orig[j]]) - tau[j];
       prod *= (j == i) ? dij : dij / (dl[i] - dl[j]);
     }
-#pragma unroll
     warp_converge();
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
     if (lane == 0) {
       const double v = sqrt(fabs(prod));
