@@ -281,6 +281,10 @@ __global__ void tgk_refine_kernel(int64_t n, const double* __restrict__ a2, doub
   if (i >= n) return;
   const double pivmin = 1e-290;
   const double s0 = sig[i] / scale;
+  // The divide & conquer value is accurate to O(eps * bound) absolutely, i.e. to
+  // O(128 eps) relatively for s0 >= bound / 128 -- zbdsqr's own relative tolerance is
+  // ~100 eps -- so only the smaller singular values are refined.
+  if (s0 >= bound * (1.0 / 128.0)) return;
   const double tau = 64.0 * DBL_EPSILON * bound;
   double lo = fmax(0.0, s0 - tau), hi = s0 + tau;
   // verify the bracket: #(sigma < lo) <= i < #(sigma < hi)
