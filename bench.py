@@ -278,7 +278,9 @@ def main():
     if panel["ms"] >= gemm["ms"]:
         ach = panel["bytes"] / (panel["ms"] / 1e3) / 1e9
         pk = peaks.get("hbm_gbs", 6650.0)
-        roofline = {"bound": "hbm", "kernel": "hetrd/gebrd cooperative panel kernel",
+        roofline = {"bound": "hbm",
+                    "kernel": ("gebrd_panel_kernel" if method == "chol-svd" else "hetrd_panel_kernel")
+                    + " (cooperative, TMA tile ring)",
                     "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk,
                     "traffic": None,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
@@ -296,8 +298,9 @@ def main():
             tr = json.load(f).get(roofline["bound"], {})
         if roofline["bound"] == "hbm" and "ratio" in tr:
             # ncu dram bytes / algorithmic bytes of one captured launch, applied per launch
-            roofline["traffic"] = tr["ratio"] * roofline["algorithmic_bytes_per_launch"]
-            roofline["traffic_source"] = tr.get("capture")
+            trk = tr.get("gebrd", tr) if method == "chol-svd" else tr
+            roofline["traffic"] = trk["ratio"] * roofline["algorithmic_bytes_per_launch"]
+            roofline["traffic_source"] = trk.get("capture")
         if roofline["bound"] == "tensor" and "bytes_per_flop" in tr:
             # ncu dram bytes per executed flop of the captured 4096^3 launch, per average launch
             roofline["traffic"] = tr["bytes_per_flop"] * gemm["flops"] / max(gemm["launches"], 1)
