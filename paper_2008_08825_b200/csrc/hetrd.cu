@@ -269,13 +269,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int cc = 0; cc < 8; ++cc) {
         const int c = 8 * warp + cc;
         const z_t a0 = tl[ring_idx(lane, c)], a1 = tl[ring_idx(lane + 32, c)];
-        z_t ar0 = a0, ar1 = a1, ac0 = a0, ac1 = a1;
-        if (diag) {  // lower triangle only; the Hermitian diagonal is real
-          ar0 = (lane > c) ? a0 : ((lane == c) ? make_double2(a0.x, 0.0) : zero);
-          ar1 = (lane + 32 > c) ? a1 : ((lane + 32 == c) ? make_double2(a1.x, 0.0) : zero);
-          ac0 = (lane > c) ? a0 : zero;
-          ac1 = (lane + 32 > c) ? a1 : zero;
-        }
+        // diagonal tiles: lower triangle only, the Hermitian diagonal real (selects, no
+        // branch: one copy of the loop body keeps the sweep's code small)
+        const bool low0 = !diag || lane > c, low1 = !diag || lane + 32 > c;
+        const bool dg0 = diag && lane == c, dg1 = diag && lane + 32 == c;
+        const z_t ac0 = low0 ? a0 : zero, ac1 = low1 ? a1 : zero;
+        const z_t ar0 = low0 ? a0 : (dg0 ? make_double2(a0.x, 0.0) : zero);
+        const z_t ar1 = low1 ? a1 : (dg1 ? make_double2(a1.x, 0.0) : zero);
         const z_t vcc = vc[c];
         zfma(r0, ar0, vcc);
         zfma(r1, ar1, vcc);
