@@ -204,14 +204,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     trace(i, 0);
     // ---------------------------------------------------------------- phase A
     const bool fwd = (i & 1) == 0;
-    // raw A(:, g) entries of a tile's row (tid < 64) / column (64 <= tid < 128) chunk
+    // Warps 4-7 own the sweep vectors (warps 0-1 finish each tile's row sums): vector thread
+    // vtid < 64 holds a tile-row entry, 64 <= vtid < 128 a tile-column entry.
+    const int vtid = tid - (kThreads - 2 * kT);
+    const bool vthr = vtid >= 0;
+    // raw A(:, g) entries of a tile's row (vtid < 64) / column (64 <= vtid < 128) chunk
     auto fetch = [&](int k) -> z_t {
       const int bi = ttab[k] & 0xffff, bj = ttab[k] >> 16;
-      const int64_t e = int64_t(sp + (tid < kT ? bi : bj)) * kT + (tid & (kT - 1));
+      const int64_t e = int64_t(sp + (vtid < kT ? bi : bj)) * kT + (vtid & (kT - 1));
       return (e > g1 && e < n) ? a.A[e + g * lda] : zero;
     };
     z_t raw = zero;
-    if (tid < 2 * kT && T > 0) raw = fetch(fwd ? 0 : T - 1);
+    if (vthr && T > 0) raw = fetch(fwd ? 0 : T - 1);
     // one warp per CTA reduces the partial norms (avoids an L2 hot spot), smem broadcast
     if (warp == 0) {
       const double xn2w = warp_sum_range(a.normp, int(g / kT), a.nch);
@@ -231,13 +235,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       a.tau[g] = tau;
     }
     trace(i, 1);
-    // v restricted to tile k's row chunk (tid < 64) / column chunk (64 <= tid < 128)
+    // v restricted to tile k's row chunk (vtid < 64) / column chunk (64 <= vtid < 128)
     auto put_v = [&](int k, z_t rw, z_t* buf) {
       const int bi = ttab[k] & 0xffff, bj = ttab[k] >> 16;
-      const int64_t e = int64_t(sp + (tid < kT ? bi : bj)) * kT + (tid & (kT - 1));
-      buf[tid] = (e == g1) ? one : ((e > g1 && e < n) ? zmul(scale, rw) : zero);
+      const int64_t e = int64_t(sp + (vtid < kT ? bi : bj)) * kT + (vtid & (kT - 1));
+      buf[vtid] = (e == g1) ? one : ((e > g1 && e < n) ? zmul(scale, rw) : zero);
     };
-    if (tid < 2 * kT && T > 0) {
+    if (vthr && T > 0) {
       put_v(fwd ? 0 : T - 1, raw, vbuf);
       raw = (T > 1) ? fetch(fwd ? 1 : T - 2) : zero;
     }
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         vrv = vr[tid];
         vcv = vc[tid];
       }
-      if (tid < 2 * kT && j + 1 < T) {  // next tile's vectors into the other buffer
+      if (vthr && j + 1 < T) {  // next tile's vectors into the other buffer
         put_v(fwd ? j + 1 : T - 2 - j, raw, vbuf + ((j + 1) & 1) * 2 * kT);
         if (j + 2 < T) raw = fetch(fwd ? j + 2 : T - 3 - j);
       }
