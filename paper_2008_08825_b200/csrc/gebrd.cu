@@ -145,9 +145,12 @@ __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const i
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
   const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
+  // warps 6-7 stage the vectors (warps 0-1 finish P4's row sums after each tile)
+  const int vtid = tid - (kThreads - kT);
+  const bool vthr = vtid >= 0;
   auto vidx = [&](int k) -> int64_t {
     const int t = ttab[k];
-    return int64_t(kCols ? (t & 0xffff) : (t >> 16)) * kT + tid;
+    return int64_t(kCols ? (t & 0xffff) : (t >> 16)) * kT + vtid;
   };
   auto fetch = [&](int k) -> z_t {
     const int64_t e = vidx(k);
@@ -156,11 +159,11 @@ __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const i
   };
   auto put = [&](int k, z_t rw, z_t* buf) {
     const int64_t e = vidx(k);
-    if (kCols) buf[tid] = (e == g) ? one : ((e > g && e < n) ? zmul(scale, rw) : zero);
-    else buf[tid] = (e == g + 1) ? one : ((e >= g + 2 && e < n) ? zmul(scale, rw) : zero);
+    if (kCols) buf[vtid] = (e == g) ? one : ((e > g && e < n) ? zmul(scale, rw) : zero);
+    else buf[vtid] = (e == g + 1) ? one : ((e >= g + 2 && e < n) ? zmul(scale, rw) : zero);
   };
   z_t raw = zero;
-  if (tid < kT && T > 0) {
+  if (vthr && T > 0) {
     put(forward ? 0 : T - 1, fetch(forward ? 0 : T - 1), vbuf);
     if (T > 1) raw = fetch(forward ? 1 : T - 2);
   }
@@ -170,7 +173,7 @@ __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const i
     const int rc = ttab[k] & 0xffff, cc = ttab[k] >> 16;
     ring.acquire(k % kRing);
     const z_t* vv = vbuf + (j & 1) * kT;
-    if (tid < kT && j + 1 < T) {  // next tile's vector into the other buffer
+    if (vthr && j + 1 < T) {  // next tile's vector into the other buffer
       put(forward ? j + 1 : T - 2 - j, raw, vbuf + ((j + 1) & 1) * kT);
       if (j + 2 < T) raw = fetch(forward ? j + 2 : T - 3 - j);
     }
