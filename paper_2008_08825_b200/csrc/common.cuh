@@ -101,7 +101,9 @@ __device__ __forceinline__ double zabs2(z_t a) { return a.x * a.x + a.y * a.y; }
 // shuffle in a diverged state (after lane-dependent branches) otherwise takes the BRA.DIV
 // fallback path, measured at ~14k cycles for a handful of shuffles in the panel kernels.
 // (A plain __syncwarp() is folded away by the compiler there; the volatile bar.warp.sync
-// stays.)
+// stays, but ptxas may still turn it into a NOP when it believes the warp converged, so the
+// panel kernels also put a CTA barrier -- WARPSYNC.ALL + BAR -- in front of warp-collective
+// blocks that follow lane-dependent code.)
 __device__ __forceinline__ void warp_converge() { asm volatile("bar.warp.sync -1;" ::: "memory"); }
 __device__ __forceinline__ double warp_sum(double v) {
   warp_converge();
@@ -128,6 +130,7 @@ __device__ __forceinline__ double warp_max(double v) {
 // Block-wide sum; `red` must hold blockDim.x/32 doubles. Result broadcast to all threads.
 __device__ inline double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();  // re-converge every warp before the butterflies (see warp_converge)
   v = warp_sum(v);
   __syncthreads();
   if (lane == 0) red[wid] = v;

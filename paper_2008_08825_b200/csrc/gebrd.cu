@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
     grid.sync();
     trace(i, 2);
     // ---------------------------------------------------------------- P2: column reflector + y'
+    __syncthreads();  // converged warps before warp 0's butterflies (BRA.DIV fallback)
     if (warp == 0) {  // one warp per CTA (no L2 hot spot), smem broadcast
       const double v = gb_warp_sum_range(a.normp, s0, a.nch);
       if (lane == 0) {
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
       }
     }
     if (cta == G - 1) {
+      __syncthreads();  // converged warps before the shuffles
       gb_tsum(a.s12, 2 * kNB, 0, s0, a.nch, V + g, ldp, i, scale, t1, kNB);
       gb_tsum(a.s12, 2 * kNB, kNB, s0, a.nch, X + g, ldp, i, scale, t2, kNB);
     }
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
     // ---------------------------------------------------------------- P4: row reflector + x'
     if (has_cols) {
       const int c0 = int((g + 1) / kT);
+      __syncthreads();  // converged warps before warp 0's butterflies
       if (warp == 0) {
         const double v = gb_warp_sum_range(a.normp, c0, a.nch);
         if (lane == 0) {
@@ -538,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
         a.taup[g] = tp;
       }
       if (cta == G - 1) {
+        __syncthreads();  // converged warps before the shuffles
         gb_tsum(a.s34, 2 * (kNB + 1), 0, c0, a.nch, Y + (g + 1), ldp, i + 1, scale2, t3, kNB + 1);
         gb_tsum(a.s34, 2 * (kNB + 1), kNB + 1, c0, a.nch, U + (g + 1), ldp, i, scale2, t4, kNB + 1);
       }
