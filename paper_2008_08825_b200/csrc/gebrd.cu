@@ -411,10 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
           V[r + int64_t(i) * ldp] = (r == g) ? make_double2(1.0, 0.0) : zmul(scale, a.A[r + g * lda]);
       }
     }
-    if (cta == G - 1) {
+    // t1 / t2 on the two last CTAs (fewest tiles, no slab), one load round each
+    if (cta == G - 1 || (cta == G - 2 && G >= 2)) {
       __syncthreads();  // converged warps before the shuffles
-      gb_tsum(a.s12, 2 * kNB, 0, s0, a.nch, V + g, ldp, i, scale, t1, kNB);
-      gb_tsum(a.s12, 2 * kNB, kNB, s0, a.nch, X + g, ldp, i, scale, t2, kNB);
+      if (cta == G - 1) gb_tsum(a.s12, 2 * kNB, 0, s0, a.nch, V + g, ldp, i, scale, t1, kNB);
+      if (cta == G - 2 || G == 1) gb_tsum(a.s12, 2 * kNB, kNB, s0, a.nch, X + g, ldp, i, scale, t2, kNB);
     }
     trace(i, 3);
     grid.sync();
@@ -540,10 +541,12 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
         a.e[g] = beta2;
         a.taup[g] = tp;
       }
-      if (cta == G - 1) {
+      if (cta == G - 1 || (cta == G - 2 && G >= 2)) {  // t3 / t4 on the two last CTAs
         __syncthreads();  // converged warps before the shuffles
-        gb_tsum(a.s34, 2 * (kNB + 1), 0, c0, a.nch, Y + (g + 1), ldp, i + 1, scale2, t3, kNB + 1);
-        gb_tsum(a.s34, 2 * (kNB + 1), kNB + 1, c0, a.nch, U + (g + 1), ldp, i, scale2, t4, kNB + 1);
+        if (cta == G - 1)
+          gb_tsum(a.s34, 2 * (kNB + 1), 0, c0, a.nch, Y + (g + 1), ldp, i + 1, scale2, t3, kNB + 1);
+        if (cta == G - 2 || G == 1)
+          gb_tsum(a.s34, 2 * (kNB + 1), kNB + 1, c0, a.nch, U + (g + 1), ldp, i, scale2, t4, kNB + 1);
       }
       if (q == 0) {
         for (int cb = gb_first_owned(c0, cta, G); cb < a.nch; cb += G) {
