@@ -42,7 +42,7 @@ static_assert(kNB % kQ == 0 && kNB <= 32, "panel width");
 // opposite directions (serpentine), each starting on the kRing tiles the previous sweep ended
 // on, and the refills stream kRing tiles ahead of the consumer.
 constexpr int kRing = 3;
-constexpr int kTabMax = 512;  // per-CTA tile list capacity (checked on the host)
+constexpr int kTabMax = 1792;  // per-CTA tile list capacity (n <= ~32k; checked on the host)
 constexpr int kTile = kT * kT;  // z_t per slot (tile_ring.cuh layout)
 }  // namespace
 

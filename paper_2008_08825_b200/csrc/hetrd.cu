@@ -103,7 +103,7 @@ __device__ __forceinline__ int first_owned(int lo, int cta, int G) {
 }
 
 constexpr int kRing = 3;
-constexpr int kTabMax = 512;  // per-CTA tile list capacity (host caps the grid accordingly)
+constexpr int kTabMax = 1280;  // per-CTA tile list capacity (n <= ~40k; checked on the host)
 using Ring = TileRing<kRing>;
 
 // Lower tile t (row-major over the triangle: (0,0), (1,0), (1,1), (2,0), ...) -> (bi, bj).
