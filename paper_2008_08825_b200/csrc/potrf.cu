@@ -1,12 +1,11 @@
 // potrf.cu — blocked right-looking Cholesky, lower (replaces LAPACKE_zpotrf 'L' at
 // proj/src/backend.cpp:51 and its NotPositiveDefinite pivot report, backend.cpp:52-56).
 //
-// Per nb = 64 block column j:
-//   1. one CTA factors the nb x nb diagonal block in shared memory (8-column warp panels +
-//      rank-8 updates), reports the first non-positive / NaN pivot (LAPACK info = j+1), and
-//      inverts L_jj (8x8 block inverses + block-wavefront products);
-//   2. panel TRSM  A21 <- A21 * L_jj^{-H}            (DMMA GEMM, in place, one CTA per row block)
-//   3. HERK update A22 <- A22 - A21 * A21^H (lower)  (DMMA GEMM, lower tiles only)
+// Per nb = 64 block column j, two launches:
+//   1. zpotrf_panel_kernel: every CTA factors the nb x nb diagonal block in shared memory,
+//      CTA 0 writes it back and reports the first non-positive / NaN pivot (LAPACK info),
+//      and each CTA solves its 32-row blocks of the panel A21 <- A21 L_jj^{-H} in place;
+//   2. HERK update A22 <- A22 - A21 * A21^H (lower)  (DMMA GEMM, lower tiles only)
 #include "blas.h"
 #include "gemm.cuh"
 
@@ -15,139 +14,195 @@ namespace bseg {
 namespace {
 constexpr int kNB = 64;
 constexpr int kLD = kNB + 1;
+constexpr int kPR = 32;  // panel rows per solve block
 }
 
-// Factor + invert one jb x jb (jb <= 64) diagonal block in shared memory.
-//  factorisation: 8 panels of 8 columns; warp 0 factors a panel (lanes own rows, no block
-//    barrier), then all 256 threads apply the rank-8 update to the trailing lower block;
-//  inverse: 8x8 diagonal-block inverses (8 warps in parallel), then the block
-//    sub-diagonals X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ one wavefront at a time.
-// Reports the first non-positive / NaN pivot as LAPACK's info (j0 + c + 1).
-__global__ void __launch_bounds__(256) zpotrf_diag_kernel(z_t* A, int64_t lda, int jb,
-                                                          int64_t j0, int* info, z_t* inv) {
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, 256;" ::"r"(id) : "memory");
+}
+
+// One block column of the right-looking Cholesky in a single launch: every CTA factors the
+// jb x jb diagonal block redundantly in shared memory (identical arithmetic, so identical
+// factors), CTA 0 writes L_jj back and reports the first non-positive / NaN pivot as LAPACK's
+// info (j0 + c + 1), and each CTA then solves its kPR-row blocks of the panel below,
+// A21 <- A21 L_jj^{-H}, by forward substitution in registers. No inverse, no second launch.
+//
+//  factorisation: warp w owns columns w, w+8, ... (register slots, rotated every 8 steps so
+//    the active column is always slot 0), lanes own rows lane and lane+32. Column c is
+//    published through a triple-buffered shared column; its producer signals named barrier
+//    1 + (c & 1) with bar.arrive and the other warps bar.sync on it. Look-ahead: the owner
+//    of column c+1 first applies column c to that one column, pivots and publishes it, and
+//    only then updates the rest of its columns, so the pivot chain (shuffle, rsqrt, scale)
+//    overlaps the other warps' rank-1 updates.
+//  panel solve: 8 threads per row (thread q owns columns q, q+8, ...), the owner of column c
+//    finishes X(r,c) and shuffles it to the 7 others, which update their columns k > c. The
+//    CTA's first row block is fetched before the factorisation starts.
+__global__ void __launch_bounds__(256, 1)
+    zpotrf_panel_kernel(z_t* A, int64_t lda, int jb, int64_t j0, int64_t rest, int* info) {
   extern __shared__ __align__(16) unsigned char sm[];
-  z_t* Ls = reinterpret_cast<z_t*>(sm);  // column-major, ld kLD
-  z_t* Xs = Ls + kNB * kLD;             // column-major, ld kLD: inverse
-  z_t* Ss = Xs + kNB * kLD;             // column-major, ld kLD: wavefront scratch
+  z_t* Ls = reinterpret_cast<z_t*>(sm);  // factor, column-major, ld kLD
+  z_t* col = Ls + kNB * kLD;             // 3 x 64 published columns
+  z_t* Bs = col + 3 * kNB;               // kPR x 64 panel rows, ld kPR + 1
+  double* rd = reinterpret_cast<double*>(Bs + kNB * (kPR + 1));  // 1 / L(c,c)
   __shared__ int failed;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) failed = (*info != 0) ? 1 : 0;  // an earlier block already failed
-  for (int e = tid; e < kNB * kNB; e += blockDim.x) {
-    const int i = e % kNB, j = e / kNB;
-    z_t v = make_double2(0.0, 0.0);
-    if (i < jb && j < jb && i >= j) v = A[i + int64_t(j) * lda];
-    if (i >= jb && i == j) v = make_double2(1.0, 0.0);  // identity padding beyond jb
-    Ls[i + j * kLD] = v;
-    Xs[i + j * kLD] = make_double2(0.0, 0.0);
-  }
+  if (tid == 0) failed = (*info != 0) ? 1 : 0;  // an earlier block column already failed
+  auto load_rows = [&](int64_t rb) {
+    const z_t* B = A + jb + rb * kPR;
+    const int rows = int(min64(kPR, rest - rb * kPR));
+    for (int e = tid; e < kPR * kNB; e += blockDim.x) {
+      const int i = e % kPR, k = e / kPR;
+      Bs[i + k * (kPR + 1)] =
+          (i < rows && k < jb) ? B[i + int64_t(k) * lda] : make_double2(0.0, 0.0);
+    }
+  };
+  if (int64_t(blockIdx.x) * kPR < rest) load_rows(blockIdx.x);
+  // registers: slot j = column warp + 8 j, rows lane (h = 0) and lane + 32 (h = 1)
+  z_t reg[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h, k = warp + 8 * j;
+      z_t v = make_double2(0.0, 0.0);
+      if (r < jb && k < jb && r >= k) v = A[r + int64_t(k) * lda];
+      if (r >= jb && r == k) v = make_double2(1.0, 0.0);  // identity padding beyond jb
+      reg[j][h] = v;
+    }
   __syncthreads();
   if (failed) return;
-  for (int p0 = 0; p0 < kNB; p0 += 8) {
-    if (warp == 0) {
-      // panel columns p0..p0+7, rows p0..63 (lanes own rows lane and lane+32)
-      for (int c = p0; c < p0 + 8; ++c) {
-        const double d = Ls[c + c * kLD].x;  // zpotf2 uses the real part of the diagonal
-        const bool bad = !(d > 0.0) && c < jb;  // also catches NaN
-        if (bad) {
-          if (lane == 0) {
-            atomicCAS(info, 0, int(j0 + c + 1));
-            failed = 1;
-          }
-          break;
-        }
-        const double l = c < jb ? sqrt(d) : 1.0;
-        const double rl = 1.0 / l;
-        __syncwarp();
+  // pivot + scale + publish of column c held in register slot `sl` of the owner warp
+  auto pivot = [&](int c, z_t (&v)[2]) {
+    warp_converge();
+    const double d = __shfl_sync(0xffffffffu, c < 32 ? v[0].x : v[1].x, c & 31);
+    // zpotf2 uses the real part of the diagonal; !(d > 0) also catches NaN (padding: d = 1)
+    if (!(d > 0.0) && lane == 0) {
+      if (blockIdx.x == 0) atomicCAS(info, 0, int(j0 + c + 1));
+      failed = 1;
+    }
+    const double rl = rsqrt(d), l = d * rl;
+    z_t* cb = col + (c % 3) * kNB;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      if (r > c) v[h] = zscale(v[h], rl);
+      if (r == c) v[h] = make_double2(l, 0.0);
+      cb[r] = v[h];
+    }
+    if (lane == 0) rd[c] = rl;
+    named_arrive(1 + (c & 1));
+  };
+  if (warp == 0) pivot(0, reg[0]);
+  for (int cc = 0; cc < 8; ++cc) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int c = 8 * cc + s;
+      const z_t* cb = col + (c % 3) * kNB;
+      if (warp != s) named_sync(1 + (c & 1));
+      else __syncwarp();
+      // look-ahead: the owner of column c+1 (warp (s+1)&7, slot ps) updates and pivots it
+      const int ps = (s == 7) ? 1 : 0;
+      const bool ahead = (warp == ((s + 1) & 7)) && (c + 1 < kNB);
+      if (ahead) {
+        const int k = c + 1;
+        const z_t y = cb[k];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = lane + 32 * h;
-          if (r > c) Ls[r + c * kLD] = zscale(Ls[r + c * kLD], rl);
+          if ((h == 1 || k < 32) && r >= k) {
+            const z_t x = cb[r];
+            z_t& v = reg[ps][h];
+            v.x -= x.x * y.x + x.y * y.y;  // v -= x conj(y)
+            v.y -= x.y * y.x - x.x * y.y;
+          }
         }
-        if (lane == 0) Ls[c + c * kLD] = make_double2(l, 0.0);
-        __syncwarp();
-        // rank-1 update of the remaining panel columns k in (c, p0+8), rows r >= k
-        for (int k = c + 1; k < p0 + 8; ++k) {
-          const z_t y = Ls[k + c * kLD];
+        pivot(k, reg[ps]);
+      }
+      // rank-1 update of the other trailing columns k > c owned by this warp
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = warp + 8 * (cc + j);
+        if (j < 8 - cc && k > c && !(ahead && j == ps)) {
+          const z_t y = cb[k];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int r = lane + 32 * h;
-            if (r >= k) {
-              const z_t x = Ls[r + c * kLD];
-              z_t v = Ls[r + k * kLD];
-              v.x -= x.x * y.x + x.y * y.y;  // v -= x conj(y)
+            if ((h == 1 || k < 32) && r >= k) {
+              const z_t x = cb[r];
+              z_t& v = reg[j][h];
+              v.x -= x.x * y.x + x.y * y.y;
               v.y -= x.y * y.x - x.x * y.y;
-              Ls[r + k * kLD] = v;
             }
           }
         }
-        __syncwarp();
       }
     }
-    __syncthreads();
-    if (failed) return;
-    // rank-8 update of the trailing lower block: A(r,k) -= sum_c L(r,c) conj(L(k,c))
-    const int t0 = p0 + 8, rem = kNB - t0;
-    for (int e = tid; e < rem * rem; e += blockDim.x) {
-      const int r = t0 + e % rem, k = t0 + e / rem;
-      if (r >= k) {
-        z_t v = Ls[r + k * kLD];
+    // slot 0 (column warp + 8 cc) is final: store it (zeros above the diagonal), rotate
+    {
+      const int k = warp + 8 * cc;
 #pragma unroll
-        for (int c = p0; c < p0 + 8; ++c) {
-          const z_t x = Ls[r + c * kLD], y = Ls[k + c * kLD];
-          v.x -= x.x * y.x + x.y * y.y;
-          v.y -= x.y * y.x - x.x * y.y;
-        }
-        Ls[r + k * kLD] = v;
+      for (int h = 0; h < 2; ++h) {
+        const int r = lane + 32 * h;
+        Ls[r + k * kLD] = (r >= k) ? reg[0][h] : make_double2(0.0, 0.0);
       }
-    }
-    __syncthreads();
-  }
-  // write the factor back (strict upper of the diagonal block zeroed)
-  for (int e = tid; e < jb * jb; e += blockDim.x) {
-    const int i = e % jb, j = e / jb;
-    A[i + int64_t(j) * lda] = (i >= j) ? Ls[i + j * kLD] : make_double2(0.0, 0.0);
-  }
-  // 8x8 diagonal-block inverses: warp w inverts block w, lane j < 8 owns column j
-  if (lane < 8) {
-    const int b0 = warp * 8, j = b0 + lane;
-    for (int i = b0; i < b0 + 8; ++i) {
-      if (i < j) continue;
-      z_t s = (i == j) ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0);
-      for (int k = j; k < i; ++k) {
-        const z_t lk = Ls[i + k * kLD], xk = Xs[k + j * kLD];
-        s.x -= lk.x * xk.x - lk.y * xk.y;
-        s.y -= lk.x * xk.y + lk.y * xk.x;
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        reg[j][0] = reg[j + 1][0];
+        reg[j][1] = reg[j + 1][1];
       }
-      const double rd = 1.0 / Ls[i + i * kLD].x;  // diagonal is real positive
-      Xs[i + j * kLD] = zscale(s, rd);
     }
   }
   __syncthreads();
-  // block sub-diagonal wavefronts d = 1..7: X_{J+d,J} = -X_II (sum_{K=J}^{I-1} L_IK X_KJ)
-  for (int d = 1; d < 8; ++d) {
-    const int nblk = 8 - d;
-    for (int e = tid; e < nblk * 64; e += blockDim.x) {
-      const int J = e / 64, ij = e % 64, ii = ij % 8, jj = ij / 8;
-      const int I = J + d;
-      const int row = I * 8 + ii, col = J * 8 + jj;
-      z_t s = make_double2(0.0, 0.0);
-      for (int k = J * 8; k < I * 8; ++k) zfma(s, Ls[row + k * kLD], Xs[k + col * kLD]);
-      Ss[row + col * kLD] = s;
+  if (failed) return;
+  if (blockIdx.x == 0)
+    for (int e = tid; e < jb * jb; e += blockDim.x) {
+      const int i = e % jb, j = e / jb;
+      A[i + int64_t(j) * lda] = Ls[i + j * kLD];
+    }
+  // panel solve X L^H = B on kPR-row blocks of A21 = A + jb
+  const int pr = tid >> 3, q = tid & 7;
+  for (int64_t rb = blockIdx.x; rb * kPR < rest; rb += gridDim.x) {
+    z_t* B = A + jb + rb * kPR;
+    const int rows = int(min64(kPR, rest - rb * kPR));
+    if (rb != blockIdx.x) {
+      __syncthreads();  // Bs reuse
+      load_rows(rb);
+      __syncthreads();
+    }
+    z_t b[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) b[m] = Bs[pr + (q + 8 * m) * (kPR + 1)];
+    for (int cc = 0; cc < 8; ++cc) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int c = 8 * cc + s;
+        z_t x = zscale(b[0], rd[c]);
+        if (q == s) b[0] = x;
+        warp_converge();
+        x.x = __shfl_sync(0xffffffffu, x.x, (lane & 24) | s);
+        x.y = __shfl_sync(0xffffffffu, x.y, (lane & 24) | s);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int k = q + 8 * (cc + m);
+          if (m < 8 - cc && k > c) {
+            const z_t y = Ls[k + c * kLD];
+            b[m].x -= x.x * y.x + x.y * y.y;  // b -= x conj(L(k,c))
+            b[m].y -= x.y * y.x - x.x * y.y;
+          }
+        }
+      }
+      Bs[pr + (q + 8 * cc) * (kPR + 1)] = b[0];
+#pragma unroll
+      for (int m = 0; m < 7; ++m) b[m] = b[m + 1];
     }
     __syncthreads();
-    for (int e = tid; e < nblk * 64; e += blockDim.x) {
-      const int J = e / 64, ij = e % 64, ii = ij % 8, jj = ij / 8;
-      const int I = J + d;
-      const int row = I * 8 + ii, col = J * 8 + jj;
-      z_t s = make_double2(0.0, 0.0);
-      for (int k = I * 8; k <= row; ++k) zfma(s, Xs[row + k * kLD], Ss[k + col * kLD]);
-      Xs[row + col * kLD] = make_double2(-s.x, -s.y);
+    for (int e = tid; e < kPR * jb; e += blockDim.x) {
+      const int i = e % kPR, k = e / kPR;
+      if (i < rows) B[i + int64_t(k) * lda] = Bs[i + k * (kPR + 1)];
     }
-    __syncthreads();
-  }
-  for (int e = tid; e < kNB * kNB; e += blockDim.x) {
-    const int i = e % kNB, j = e / kNB;
-    inv[i + j * kNB] = (i < jb && j < jb) ? Xs[i + j * kLD] : make_double2(0.0, 0.0);
   }
 }
 
@@ -162,27 +217,27 @@ __global__ void zero_strict_upper_kernel(int64_t n, z_t* A, int64_t lda) {
 
 void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z_t* ws,
                   bool zero_upper) {
-  const size_t smem = size_t(3) * kNB * kLD * sizeof(z_t);
+  (void)ws;  // kept for the call sites' workspace contract; the panel kernel needs none
+  const size_t smem = size_t(kNB * kLD + 3 * kNB + kNB * (kPR + 1)) * sizeof(z_t) +
+                      kNB * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    BSE_CUDA(cudaFuncSetAttribute(zpotrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(smem)));
+    BSE_CUDA(cudaFuncSetAttribute(zpotrf_panel_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = true;
   }
   BSE_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), s));
-  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
+  const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
   for (int64_t j = 0; j < n; j += kNB) {
     const int jb = int(min64(kNB, n - j));
     z_t* Ajj = A + j + j * lda;
-    zpotrf_diag_kernel<<<1, 256, smem, s>>>(Ajj, lda, jb, j, d_info, ws);
-    BSE_LAUNCH_CHECK();
     const int64_t rest = n - j - jb;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(rest, kPR))));
+    zpotrf_panel_kernel<<<grid, 256, smem, s>>>(Ajj, lda, jb, j, rest, d_info);
+    BSE_LAUNCH_CHECK();
     if (rest <= 0) break;
+    // HERK update A22 <- A22 - A21 A21^H (lower tiles only)
     z_t* A21 = A + (j + jb) + j * lda;
-    // A21 <- A21 * inv(L_jj)^H : in place is safe because one CTA owns a full row block
-    // (jb <= BN) and reads all of it before its epilogue writes.
-    zgemm(s, 0, 1, rest, jb, jb, one, A21, lda, ws, kNB, zero, A21, lda, kGeneral, kUpperOp, 0,
-          nullptr, 0);
     z_t* A22 = A + (j + jb) + (j + jb) * lda;
     zgemm(s, 0, 1, rest, rest, jb, mone, A21, lda, A21, lda, one, A22, lda, kGeneral, kGeneral, 1,
           nullptr, 0);
