@@ -236,6 +236,7 @@ def main():
     # ---- end to end through the host-pointer C-ABI (bse_solve): H2D + solve + D2H per step
     e2e = None
     if not args.no_e2e:
+        ctx.set_kernel_timing(False)  # the user-facing call runs without per-kernel events
         hv = torch.empty((n, 2 * n), dtype=torch.complex128).pin_memory()
         hl = torch.empty(n, dtype=torch.float64).pin_memory()
         import ctypes
@@ -243,6 +244,17 @@ def main():
         st = bse.Status()
         ns = np.zeros(n, dtype=np.int64)
         nn = ctypes.c_int64(0)
+
+        def host_solve(ha, hb):
+            return L.bse_solve(ctx.handle, int(meth), n, ctypes.c_void_p(ha.data_ptr()), n,
+                               ctypes.c_void_p(hb.data_ptr()), n, ctypes.c_void_p(hl.data_ptr()),
+                               ctypes.c_void_p(hv.data_ptr()), 2 * n,
+                               ns.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nn),
+                               ctypes.byref(st))
+
+        for k in range(args.warmup):  # untimed: staging buffers, sink streams, first touches
+            if host_solve(*host[k]) != 0:
+                raise RuntimeError(st.message.decode())
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -250,12 +262,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for k in range(args.steps):
-            ha, hb = host[args.warmup + k]
-            rc = L.bse_solve(ctx.handle, int(meth), n, ctypes.c_void_p(ha.data_ptr()), n,
-                             ctypes.c_void_p(hb.data_ptr()), n, ctypes.c_void_p(hl.data_ptr()),
-                             ctypes.c_void_p(hv.data_ptr()), 2 * n,
-                             ns.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nn), ctypes.byref(st))
-            if rc != 0:
+            if host_solve(*host[args.warmup + k]) != 0:
                 raise RuntimeError(st.message.decode())
         e1.record(stream)
         torch.cuda.synchronize()

@@ -164,6 +164,30 @@ void run_solve(bse_ctx* c, int method, int64_t n, const z_t* A, int64_t lda, con
   else throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "unknown method"};
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Installs the host sink for one bse_solve call; always cleared, also on a DomainError.
+struct SinkScope {
+  bse_ctx* c;
+  SinkScope(bse_ctx* ctx, double* v, int64_t ldv) : c(ctx) {
+    c->sink_v = v;
+    c->sink_ldv = ldv;
+    c->sink_k = 0;
+  }
+  ~SinkScope() {
+    if (c->sink_v && c->sink_k > 0) cudaStreamSynchronize(c->copy);
+    c->sink_v = nullptr;
+    c->sink_k = 0;
+  }
+};
+
 void check_dims(int64_t n, int64_t lda, int64_t ldb) {
   if (n < 1) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "blocks must be at least 1x1"};
   if (lda < n || ldb < n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "leading dimension too small"};
@@ -193,6 +217,13 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
     BSE_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     BSE_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     BSE_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    BSE_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    // keep the stream-ordered staging buffers of bse_solve mapped between calls
+    cudaMemPool_t pool;
+    BSE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    BSE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    for (auto& ev : c->sink_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : c->ev) BSE_CUDA(cudaEventCreate(&ev));
   } catch (const CudaError& ex) {
     delete c;
@@ -214,6 +245,12 @@ int bse_ctx_destroy(bse_ctx* c) {
     cudaStreamSynchronize(c->aux);
     cudaStreamDestroy(c->aux);
   }
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+  }
+  for (auto& ev : c->sink_ev)
+    if (ev) cudaEventDestroy(ev);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -289,11 +326,14 @@ int bse_solve(bse_ctx* c, int method, int64_t n, const double* a, int64_t lda, c
     h2d(c, dA, n, a, lda, n, n);
     h2d(c, dB, n, b, ldb, n, n);
     std::vector<int64_t> flagged;
+    // Page-locked output: the solver streams finished column chunks of V to it on the copy
+    // stream while it computes the next ones. Pageable output is copied after the solve.
+    SinkScope sink(c, is_pinned(v) ? v : nullptr, ldv);
     run_solve(c, method, n, dA, n, dB, n, dL, dV, 2 * n, flagged);
     collect_timer(c);
     BSE_CUDA(cudaMemcpyAsync(lambda, dL, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
                              c->stream));
-    d2h(c, v, ldv, dV, 2 * n, 2 * n, n);
+    if (!sink_finish(c)) d2h(c, v, ldv, dV, 2 * n, 2 * n, n);
     BSE_CUDA(cudaStreamSynchronize(c->stream));
     if (n_near_singular) *n_near_singular = int64_t(flagged.size());
     if (near_singular)

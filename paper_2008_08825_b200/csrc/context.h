@@ -23,6 +23,13 @@ struct bse_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> timer_events;
   bseg::KernelTimer timer;
+  // streamed eigenvector output (bse_solve into pinned host memory): the recovery stage
+  // copies finished column chunks of V to sink_v on `copy` while later chunks compute
+  cudaStream_t copy = nullptr;
+  cudaEvent_t sink_ev[17]{};
+  double* sink_v = nullptr;
+  int64_t sink_ldv = 0;
+  int sink_k = 0;
 };
 
 namespace bseg {
@@ -63,6 +70,14 @@ struct DomainError {
   int64_t pivot;
   std::string msg;
 };
+
+// Column chunk width for the recovery stage: the whole matrix unless a host sink is set.
+int64_t recover_chunk_cols(const bse_ctx* c, int64_t n, int64_t min_cols, int parts);
+// Queues the D2H of columns [j0, j0+jb) of V (2n x n, ld ldv) to the host sink (no-op
+// without a sink) on the copy stream, ordered after everything enqueued on c->stream.
+void sink_columns(bse_ctx* c, const z_t* V, int64_t ldv, int64_t n, int64_t j0, int64_t jb);
+// Main stream waits for the sink copies; returns true when the whole V was streamed.
+bool sink_finish(bse_ctx* c);
 
 // Solver pipelines on device pointers (solvers.cu). Throw DomainError / CudaError.
 void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t* B,

@@ -8,6 +8,7 @@
 // product_pair's definiteness certificates (core.cpp:87-100) keep their order and error
 // payloads; the certificate factor of A-B (CHOL) and both factors (CHOL+SVD) are reused
 // instead of recomputed (the reference runs potrf 3x / 4x).
+#include <cstdlib>
 #include <cstring>
 
 #include "blas.h"
@@ -34,6 +35,39 @@ struct PhaseClock {
     return ms;
   }
 };
+
+}  // namespace
+
+int64_t recover_chunk_cols(const bse_ctx* c, int64_t n, int64_t min_cols, int parts) {
+  static const char* force = std::getenv("BSE_FORCE_CHUNKS");  // experiments: chunk w/o sink
+  static const char* ep = std::getenv("BSE_CHUNK_PARTS");
+  static const char* em = std::getenv("BSE_CHUNK_MIN");
+  if (ep) parts = std::atoi(ep);
+  if (em) min_cols = std::atoi(em);
+  if (!c->sink_v && !force) return n;
+  const int64_t w = std::max<int64_t>(min_cols, ceil_div(ceil_div(n, parts), 64) * 64);
+  return std::min<int64_t>(n, w);
+}
+
+void sink_columns(bse_ctx* c, const z_t* V, int64_t ldv, int64_t n, int64_t j0, int64_t jb) {
+  if (!c->sink_v || jb <= 0) return;
+  if (c->sink_k >= 16) throw std::runtime_error("too many sink chunks");
+  cudaEvent_t ev = c->sink_ev[c->sink_k++];
+  BSE_CUDA(cudaEventRecord(ev, c->stream));
+  BSE_CUDA(cudaStreamWaitEvent(c->copy, ev, 0));
+  BSE_CUDA(cudaMemcpy2DAsync(c->sink_v + 2 * j0 * c->sink_ldv, size_t(c->sink_ldv) * sizeof(z_t),
+                             V + j0 * ldv, size_t(ldv) * sizeof(z_t), size_t(2 * n) * sizeof(z_t),
+                             size_t(jb), cudaMemcpyDeviceToHost, c->copy));
+}
+
+bool sink_finish(bse_ctx* c) {
+  if (!c->sink_v || c->sink_k == 0) return false;
+  BSE_CUDA(cudaEventRecord(c->sink_ev[16], c->copy));
+  BSE_CUDA(cudaStreamWaitEvent(c->stream, c->sink_ev[16], 0));
+  return true;
+}
+
+namespace {
 
 std::string pivot_msg(int info) {
   return "leading minor of order " + std::to_string(info) + " is not positive definite";
@@ -150,16 +184,24 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   }
   // lambda_from_squares (solvers.cpp:125)
   clamp_spectrum(s, n, d, 0, lam, flg, nonpos, counts, floor_p);
-  // V1 = L^{-H} V_M (solvers.cpp:127) in b3 (aux stream) ; V2 = L V_M (solvers.cpp:128) in b0
-  fork(c);
-  zcopy2d(c->aux, n, n, b2, ld, b3, ld);
-  ztrsm_lower(c->aux, 0, 1, n, n, b1, ld, b3, ld, ws_trsm, 64);
-  zgemm(s, 0, 0, n, n, n, kOne, b1, ld, b2, ld, kZero, b0, ld, kLowerOp, kGeneral, 0, nullptr, 0);
-  join(c);
-  // assemble with (lambda^2, 1) (solvers.cpp:130-133) + breakdown rebuild
-  // l1 = lambda^2 (after clamping), l2 = 1
+  // l1 = lambda^2 (after clamping), l2 = 1 for the assembly below
   square_vec(s, n, lam, l1);
-  assemble(s, n, n, b3, ld, b0, ld, l1, nullptr, 1, d, floor_p, V, ldv);
+  // V1 = L^{-H} V_M (solvers.cpp:127) in b3 (aux stream) ; V2 = L V_M (solvers.cpp:128) in b0;
+  // in column chunks when V streams to a host sink, so chunk q's copy overlaps chunk q+1
+  const int64_t cw = recover_chunk_cols(c, n, 512, 2);
+  for (int64_t j0 = 0; j0 < n; j0 += cw) {
+    const int64_t jb = std::min<int64_t>(cw, n - j0);
+    fork(c);
+    zcopy2d(c->aux, n, jb, b2 + j0 * ld, ld, b3 + j0 * ld, ld);
+    ztrsm_lower(c->aux, 0, 1, n, jb, b1, ld, b3 + j0 * ld, ld, ws_trsm, 64);
+    zgemm(s, 0, 0, n, jb, n, kOne, b1, ld, b2 + j0 * ld, ld, kZero, b0 + j0 * ld, ld, kLowerOp,
+          kGeneral, 0, nullptr, 0);
+    join(c);
+    // assemble with (lambda^2, 1) (solvers.cpp:130-133) + breakdown rebuild
+    assemble(s, n, jb, b3 + j0 * ld, ld, b0 + j0 * ld, ld, l1 + j0, nullptr, 1, d + j0, floor_p,
+             V + j0 * ldv, ldv);
+    sink_columns(c, V, ldv, n, j0, jb);
+  }
   clk.mark();
   read_flags(c, n, counts, flg, flagged, "squared-problem spectrum has no positive eigenvalue");
   bse_phase_times& t = c->last;
@@ -245,13 +287,23 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   }
   // clamp_singular_ascending (solvers.cpp:145); s already ascending (no column reversal)
   clamp_spectrum(s, n, sasc, 1, lam, flg, nonpos, counts, floor_p);
-  // V1 = L1 U diag(lam^-1/2) -> b2 ; V2 = L2 V diag(lam^-1/2) -> b0 (L1 no longer needed after)
-  zgemm(s, 0, 0, n, n, n, kOne, b0, ld, b3, ld, kZero, b2, ld, kLowerOp, kGeneral, 0, nullptr, 0);
-  zgemm(s, 0, 0, n, n, n, kOne, b1, ld, b4, ld, kZero, b0, ld, kLowerOp, kGeneral, 0, nullptr, 0);
-  scale_cols_rsqrt(s, n, n, b2, ld, lam);
-  scale_cols_rsqrt(s, n, n, b0, ld, lam);
-  // assemble with (lambda, lambda) -> unit scalings (solvers.cpp:158-160)
-  assemble(s, n, n, b2, ld, b0, ld, lam, lam, 0, nullptr, floor_p, V, ldv);
+  // V1 = L1 U diag(lam^-1/2) -> b2 ; V2 = L2 V diag(lam^-1/2) -> X (free after the extract);
+  // in column chunks when V streams to a host sink
+  z_t* v2 = reinterpret_cast<z_t*>(X);
+  const int64_t cw = recover_chunk_cols(c, n, 512, 2);
+  for (int64_t j0 = 0; j0 < n; j0 += cw) {
+    const int64_t jb = std::min<int64_t>(cw, n - j0);
+    zgemm(s, 0, 0, n, jb, n, kOne, b0, ld, b3 + j0 * ld, ld, kZero, b2 + j0 * ld, ld, kLowerOp,
+          kGeneral, 0, nullptr, 0);
+    zgemm(s, 0, 0, n, jb, n, kOne, b1, ld, b4 + j0 * ld, ld, kZero, v2 + j0 * ld, ld, kLowerOp,
+          kGeneral, 0, nullptr, 0);
+    scale_cols_rsqrt(s, n, jb, b2 + j0 * ld, ld, lam + j0);
+    scale_cols_rsqrt(s, n, jb, v2 + j0 * ld, ld, lam + j0);
+    // assemble with (lambda, lambda) -> unit scalings (solvers.cpp:158-160)
+    assemble(s, n, jb, b2 + j0 * ld, ld, v2 + j0 * ld, ld, lam + j0, lam + j0, 0, nullptr,
+             floor_p, V + j0 * ldv, ldv);
+    sink_columns(c, V, ldv, n, j0, jb);
+  }
   clk.mark();
   read_flags(c, n, counts, flg, flagged, "singular spectrum is identically zero");
   bse_phase_times& t = c->last;

@@ -247,3 +247,39 @@ def test_device_diagnostics_through_torch_buffers():
     assert np.array_equal(out.cpu().numpy(), bse.residual(h, r))  # deterministic, same kernels
     s = bse.sigma_orthogonality_error_device(600, 300, dv.data_ptr())
     assert s == bse.sigma_orthogonality_error(r.v)
+
+
+# ------------------------------------------------- streamed output into page-locked host memory
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+@pytest.mark.parametrize("n", [700, 1500])
+def test_pinned_output_streams_same_solution(method, n):
+    """bse_solve into page-locked buffers copies V in column chunks while the recovery stage
+    is still running (solvers.cu sink_columns); the result must match the pageable path."""
+    import ctypes
+
+    import torch
+
+    a, b = configs.config2(5, n=n)
+    ref = bse.solve(method, bse.from_blocks(a, b))  # numpy (pageable) output path
+    ha = torch.from_numpy(np.asfortranarray(a).T.copy()).pin_memory()
+    hb = torch.from_numpy(np.asfortranarray(b).T.copy()).pin_memory()
+    hv = torch.full((n, 2 * n), complex("nan"), dtype=torch.complex128).pin_memory()
+    hl = torch.empty(n, dtype=torch.float64).pin_memory()
+    ctx = bse.default_context()
+    lib = bse._lib.lib()
+    st = bse.Status()
+    ns = np.zeros(n, dtype=np.int64)
+    nn = ctypes.c_int64(0)
+    rc = lib.bse_solve(ctx.handle, int(method), n, ctypes.c_void_p(ha.data_ptr()), n,
+                       ctypes.c_void_p(hb.data_ptr()), n, ctypes.c_void_p(hl.data_ptr()),
+                       ctypes.c_void_p(hv.data_ptr()), 2 * n, ns.ctypes.data_as(ctypes.c_void_p),
+                       ctypes.byref(nn), ctypes.byref(st))
+    assert rc == 0, st.message
+    lam = hl.numpy()
+    v = hv.numpy().T  # (2n, n) column-major view
+    assert np.array_equal(lam, ref.lambda_)
+    assert np.all(np.isfinite(v))
+    scale = np.abs(ref.v).max()
+    assert np.abs(v - ref.v).max() <= 1e-9 * scale
+    res = residual(a, b, lam, v)
+    assert res.max() <= 100 * n * EPS
