@@ -131,6 +131,20 @@ int bse_solve_device(bse_ctx* ctx, int method, int64_t n,
                      double* d_lambda, double* d_v, int64_t ldv,
                      int64_t* near_singular, int64_t* n_near_singular, bse_status* st);
 
+/* Batch driver: solves `batch` independent matrices with the same
+ * method and shape from host buffers a[i], b[i] into lambda[i], v[i]. The upload of matrix
+ * i+1 and the download of matrix i-1 run on copy streams while matrix i computes, so with
+ * page-locked host buffers the PCIe traffic hides behind the solves.
+ *   near_singular  : null or capacity batch*n (row i holds matrix i's flagged indices)
+ *   n_near_singular: null or capacity batch
+ *   failed_index   : null or receives the first failing item (-1 when all succeed); the
+ *                    error payload in st is that item's, earlier items' outputs are valid */
+int bse_solve_batched(bse_ctx* ctx, int method, int64_t n, int64_t batch,
+                      const double* const* a, int64_t lda, const double* const* b, int64_t ldb,
+                      double* const* lambda, double* const* v, int64_t ldv,
+                      int64_t* near_singular, int64_t* n_near_singular, int64_t* failed_index,
+                      bse_status* st);
+
 /* ---------------------------------------------------------------- core glue (core.cpp) */
 /* product_pair (core.cpp:87-100): m1 = a+b, m2 = a-b, each certified by Cholesky.     */
 int bse_product_pair(bse_ctx* ctx, int64_t n, const double* a, int64_t lda,

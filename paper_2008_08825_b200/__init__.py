@@ -33,7 +33,7 @@ __all__ = [
     "ConvergenceFailure", "SingularFactor", "NonPositiveScale", "InvalidSpec", "DeviceError",
     "from_blocks", "product_pair", "assemble_eigenvectors", "solve_chol", "solve_chol_svd",
     "solve", "negative_spectrum", "hermitian_eig", "cholesky_lower", "svd", "tri_solve", "matmul",
-    "solve_sqrt", "solve_reference", "hpd_sqrt", "residual", "sigma_orthogonality_error",
+    "solve_sqrt", "solve_reference", "solve_batched", "BatchError", "hpd_sqrt", "residual", "sigma_orthogonality_error",
     "check_form1", "check_form2", "check_pairing", "predicted_error", "OddDimension",
     "residual_device", "sigma_orthogonality_error_device",
     "LengthMismatch",
@@ -395,6 +395,53 @@ def solve(method: Method, h: BseMatrixI, ctx: Optional[Context] = None) -> Spect
     if int(method) not in (0, 1, 2, 3):
         raise InvalidSpec("unknown method")
     return _solve(Method(method), h, ctx)
+
+
+class BatchError(Error):
+    """A bse_solve_batched item failed: `index` is the item, `error` its typed exception
+    (the payload classes above); `results` holds the items solved before it."""
+
+    def __init__(self, index: int, error: Error, results: List[SpectralResult]):
+        super().__init__(str(error))
+        self.index, self.error, self.results = index, error, results
+
+
+def solve_batched(method: Method, hs: List[BseMatrixI],
+                  ctx: Optional[Context] = None) -> List[SpectralResult]:
+    """Config-5 batch driver: the same method over independent matrices of one
+    size through bse_solve_batched, which overlaps the next upload and the previous download
+    with each solve (fully so for page-locked buffers; numpy arrays are pageable)."""
+    ctx = ctx or default_context()
+    if int(method) not in (0, 1, 2, 3):
+        raise InvalidSpec("unknown method")
+    if not hs:
+        return []
+    n = hs[0].n
+    if any(h.n != n for h in hs):
+        raise DimensionMismatch("batch items must share one size")
+    k = len(hs)
+    lams = [np.zeros(n) for _ in range(k)]
+    vs = [np.zeros((2 * n, n), dtype=np.complex128, order="F") for _ in range(k)]
+    ptrs = lambda arrs: (ctypes.c_void_p * k)(*[a.ctypes.data for a in arrs])  # noqa: E731
+    pa, pb = ptrs([h.a for h in hs]), ptrs([h.b for h in hs])
+    pl, pv = ptrs(lams), ptrs(vs)
+    ns = np.zeros((k, n), dtype=np.int64)
+    nn = np.zeros(k, dtype=np.int64)
+    failed = ctypes.c_int64(-1)
+    st = Status()
+    rc = _lib.lib().bse_solve_batched(ctx.handle, int(method), n, k, pa, n, pb, n, pl, pv, 2 * n,
+                                      _p(ns), _p(nn), ctypes.byref(failed), ctypes.byref(st))
+    done = failed.value if rc != 0 and failed.value >= 0 else (k if rc == 0 else 0)
+    out = [SpectralResult(lams[i], vs[i], Method(method), [int(j) for j in ns[i, : nn[i]]])
+           for i in range(done)]
+    if rc != 0:
+        try:
+            _check(rc, st)
+        except Error as e:
+            if failed.value >= 0:
+                raise BatchError(failed.value, e, out) from e
+            raise
+    return out
 
 
 def negative_spectrum(h: BseMatrixI, r: SpectralResult,

@@ -245,6 +245,35 @@ SpectralResult solve_sqrt(const BseMatrixI& h) { return run(Method::Sqrt, h); }
 SpectralResult solve_reference(const BseMatrixI& h) { return run(Method::Reference, h); }
 SpectralResult solve(Method method, const BseMatrixI& h) { return run(method, h); }
 
+std::vector<SpectralResult> solve_batched(Method method, const std::vector<BseMatrixI>& hs) {
+  std::vector<SpectralResult> out(hs.size());
+  if (hs.empty()) return out;
+  const Index n = hs[0].n();
+  for (const auto& h : hs)
+    if (h.n() != n) throw DimensionMismatch("solve_batched: batch items must share one size");
+  const size_t k = hs.size();
+  std::vector<const double*> pa(k), pb(k);
+  std::vector<double*> pl(k), pv(k);
+  for (size_t i = 0; i < k; ++i) {
+    out[i].method = method;
+    out[i].lambda.assign(static_cast<size_t>(n), 0.0);
+    out[i].v = Matrix(2 * n, n);
+    pa[i] = dp(hs[i].a());
+    pb[i] = dp(hs[i].b());
+    pl[i] = out[i].lambda.data();
+    pv[i] = dp(out[i].v);
+  }
+  std::vector<int64_t> ns(k * static_cast<size_t>(n)), nn(k);
+  int64_t failed = -1;
+  bse_status st{};
+  check(bse_solve_batched(ctx(), static_cast<int>(method), n, int64_t(k), pa.data(), n, pb.data(),
+                          n, pl.data(), pv.data(), 2 * n, ns.data(), nn.data(), &failed, &st),
+        st);
+  for (size_t i = 0; i < k; ++i)
+    out[i].near_singular.assign(ns.begin() + i * n, ns.begin() + i * n + nn[i]);
+  return out;
+}
+
 SpectralResult negative_spectrum(const BseMatrixI& h, const SpectralResult& r) {
   const Index n = h.n();
   if (r.v.rows() != 2 * n || r.v.cols() != Index(r.lambda.size()))

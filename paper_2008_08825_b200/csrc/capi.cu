@@ -218,6 +218,8 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
     BSE_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     BSE_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     BSE_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    BSE_CUDA(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+    for (auto& ev : c->batch_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     // keep the stream-ordered staging buffers of bse_solve mapped between calls
     cudaMemPool_t pool;
     BSE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -250,6 +252,12 @@ int bse_ctx_destroy(bse_ctx* c) {
     cudaStreamDestroy(c->copy);
   }
   for (auto& ev : c->sink_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->copy_in) {
+    cudaStreamSynchronize(c->copy_in);
+    cudaStreamDestroy(c->copy_in);
+  }
+  for (auto& ev : c->batch_ev)
     if (ev) cudaEventDestroy(ev);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
@@ -338,6 +346,89 @@ int bse_solve(bse_ctx* c, int method, int64_t n, const double* a, int64_t lda, c
     if (n_near_singular) *n_near_singular = int64_t(flagged.size());
     if (near_singular)
       for (size_t i = 0; i < flagged.size(); ++i) near_singular[i] = flagged[i];
+  });
+}
+
+int bse_solve_batched(bse_ctx* c, int method, int64_t n, int64_t batch, const double* const* a,
+                      int64_t lda, const double* const* b, int64_t ldb, double* const* lambda,
+                      double* const* v, int64_t ldv, int64_t* near_singular,
+                      int64_t* n_near_singular, int64_t* failed_index, bse_status* st) {
+  if (failed_index) *failed_index = -1;
+  return guarded(c, st, [&] {
+    check_dims(n, lda, ldb);
+    if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
+    if (batch < 0) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "negative batch"};
+    if (batch == 0) return;
+    if (!a || !b || !lambda || !v)
+      throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "null batch pointer array"};
+    const size_t nn = size_t(n) * size_t(n);
+    // two slots of (A, B, V, lambda): matrix i+1 uploads and matrix i-1 downloads while
+    // matrix i computes (copy-in on c->copy_in, copy-out on c->copy, compute on c->stream)
+    const size_t slot = 2 * nn + 2 * nn + size_t(n) / 2 + 64;  // in z_t units
+    DevBuf buf(2 * slot * sizeof(z_t), c->stream);
+    z_t *dA[2], *dB[2], *dV[2];
+    double* dL[2];
+    for (int k = 0; k < 2; ++k) {
+      z_t* base = buf.as<z_t>() + k * slot;
+      dA[k] = base;
+      dB[k] = base + nn;
+      dV[k] = base + 2 * nn;
+      dL[k] = reinterpret_cast<double*>(base + 4 * nn);
+    }
+    struct Drain {  // the copy streams finish before the staging buffers are released
+      bse_ctx* c;
+      ~Drain() {
+        cudaStreamSynchronize(c->copy_in);
+        cudaStreamSynchronize(c->copy);
+      }
+    } drain{c};
+    cudaEvent_t* in_ready = c->batch_ev;       // [2] copy_in -> compute
+    cudaEvent_t* comp_done = c->batch_ev + 2;  // [2] compute -> copy_in / copy
+    cudaEvent_t* out_done = c->batch_ev + 4;   // [2] copy -> compute (slot reuse)
+    auto upload = [&](int64_t i) {
+      const int k = int(i & 1);
+      if (i >= 2) BSE_CUDA(cudaStreamWaitEvent(c->copy_in, comp_done[k], 0));
+      BSE_CUDA(cudaMemcpy2DAsync(dA[k], size_t(n) * sizeof(z_t), a[i], size_t(lda) * sizeof(z_t),
+                                 size_t(n) * sizeof(z_t), size_t(n), cudaMemcpyHostToDevice,
+                                 c->copy_in));
+      BSE_CUDA(cudaMemcpy2DAsync(dB[k], size_t(n) * sizeof(z_t), b[i], size_t(ldb) * sizeof(z_t),
+                                 size_t(n) * sizeof(z_t), size_t(n), cudaMemcpyHostToDevice,
+                                 c->copy_in));
+      BSE_CUDA(cudaEventRecord(in_ready[k], c->copy_in));
+    };
+    // the staging allocation is ordered on c->stream; the copy-in stream starts after it
+    BSE_CUDA(cudaEventRecord(c->batch_ev[6], c->stream));
+    BSE_CUDA(cudaStreamWaitEvent(c->copy_in, c->batch_ev[6], 0));
+    upload(0);
+    for (int64_t i = 0; i < batch; ++i) {
+      const int k = int(i & 1);
+      if (i + 1 < batch) upload(i + 1);
+      BSE_CUDA(cudaStreamWaitEvent(c->stream, in_ready[k], 0));
+      if (i >= 2) BSE_CUDA(cudaStreamWaitEvent(c->stream, out_done[k], 0));
+      std::vector<int64_t> flagged;
+      if (c->timing) c->timer.used = 0;
+      try {
+        run_solve(c, method, n, dA[k], n, dB[k], n, dL[k], dV[k], 2 * n, flagged);
+      } catch (DomainError& e) {
+        if (failed_index) *failed_index = i;
+        e.msg = "batch item " + std::to_string(i) + ": " + e.msg;
+        throw;
+      }
+      collect_timer(c);
+      BSE_CUDA(cudaEventRecord(comp_done[k], c->stream));
+      BSE_CUDA(cudaStreamWaitEvent(c->copy, comp_done[k], 0));
+      BSE_CUDA(cudaMemcpyAsync(lambda[i], dL[k], sizeof(double) * size_t(n),
+                               cudaMemcpyDeviceToHost, c->copy));
+      BSE_CUDA(cudaMemcpy2DAsync(v[i], size_t(ldv) * sizeof(z_t), dV[k],
+                                 size_t(2 * n) * sizeof(z_t), size_t(2 * n) * sizeof(z_t),
+                                 size_t(n), cudaMemcpyDeviceToHost, c->copy));
+      BSE_CUDA(cudaEventRecord(out_done[k], c->copy));
+      if (n_near_singular) n_near_singular[i] = int64_t(flagged.size());
+      if (near_singular)
+        for (size_t f = 0; f < flagged.size(); ++f) near_singular[i * n + int64_t(f)] = flagged[f];
+    }
+    BSE_CUDA(cudaStreamSynchronize(c->copy));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -30,6 +30,9 @@ struct bse_ctx {
   double* sink_v = nullptr;
   int64_t sink_ldv = 0;
   int sink_k = 0;
+  // bse_solve_batched: host-to-device uploads of the next matrix run on copy_in
+  cudaStream_t copy_in = nullptr;
+  cudaEvent_t batch_ev[7]{};
 };
 
 namespace bseg {

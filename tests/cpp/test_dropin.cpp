@@ -39,6 +39,22 @@ int main() {
     const SpectralResult r = solve_chol(from_blocks(a, Matrix::Zero(3, 3)));
     CHECK(std::abs(r.lambda[0] - 1.0) < 1e-13 && std::abs(r.lambda[2] - 3.0) < 1e-13);
   }
+  {  // batch driver: items equal the single solves; the failing item's class is thrown
+    std::vector<BseMatrixI> hs{from_blocks(scalar(2.0), scalar(1.0)),
+                               from_blocks(scalar(5.0), scalar(3.0))};
+    const auto rs = solve_batched(Method::Chol, hs);
+    CHECK(rs.size() == 2);
+    CHECK(std::abs(rs[0].lambda[0] - s3) < 1e-13 * s3);
+    CHECK(std::abs(rs[1].lambda[0] - 4.0) < 1e-13 * 4.0);  // sqrt(5^2 - 3^2)
+    hs.push_back(from_blocks(scalar(1.0), scalar(2.0)));
+    try {
+      solve_batched(Method::Chol, hs);
+      CHECK(false);
+    } catch (const NotDefinite& e) {
+      CHECK(e.which() == Block::M2);
+      CHECK(std::string(e.what()).find("batch item 2") != std::string::npos);
+    }
+  }
   try {  // test_solvers.cpp:73-79
     solve_chol_svd(from_blocks(scalar(1.0), scalar(2.0)));
     CHECK(false);

@@ -283,3 +283,64 @@ def test_pinned_output_streams_same_solution(method, n):
     assert np.abs(v - ref.v).max() <= 1e-9 * scale
     res = residual(a, b, lam, v)
     assert res.max() <= 100 * n * EPS
+
+
+# ------------------------------------------------------------- batch driver
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+def test_solve_batched_matches_single_solves(method):
+    hs = [bse.from_blocks(*configs.config2(s, n=n)) for s, n in ((0, 150), (1, 150), (2, 150))]
+    out = bse.solve_batched(method, hs)
+    assert len(out) == 3
+    for h, r in zip(hs, out):
+        one = bse.solve(method, h)  # same kernels on the same inputs: bit-identical
+        assert np.array_equal(r.lambda_, one.lambda_)
+        assert np.array_equal(r.v, one.v)
+        assert r.near_singular == one.near_singular and r.method == method
+
+
+def test_solve_batched_reports_failing_item():
+    n = 40
+    good = bse.from_blocks(*configs.config2(4, n=n))
+    a = np.eye(n, dtype=complex)
+    bad = bse.from_blocks(a, 2 * a)  # A - B = -I: M2 not definite
+    with pytest.raises(bse.BatchError) as ei:
+        bse.solve_batched(bse.Method.Chol, [good, bad, good])
+    assert ei.value.index == 1
+    assert isinstance(ei.value.error, bse.NotDefinite)
+    assert ei.value.error.which == bse.Block.M2
+    assert len(ei.value.results) == 1
+    assert np.array_equal(ei.value.results[0].lambda_, bse.solve_chol(good).lambda_)
+    with pytest.raises(bse.DimensionMismatch):
+        bse.solve_batched(bse.Method.Chol, [good, bse.from_blocks(*configs.config2(0, n=30))])
+    assert bse.solve_batched(bse.Method.Chol, []) == []
+
+
+def test_solve_batched_pinned_overlap():
+    """Page-locked batch: uploads/downloads overlap the solves; results equal single solves."""
+    import ctypes
+
+    import torch
+
+    n, k = 1100, 3
+    hs = [bse.from_blocks(*configs.config2(10 + s, n=n)) for s in range(k)]
+    mats = [(h.a, h.b) for h in hs]
+    pin = lambda x: torch.from_numpy(np.asfortranarray(x).T.copy()).pin_memory()  # noqa: E731
+    ha = [pin(a) for a, _ in mats]
+    hb = [pin(b) for _, b in mats]
+    hv = [torch.empty((n, 2 * n), dtype=torch.complex128).pin_memory() for _ in range(k)]
+    hl = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(k)]
+    arr = lambda ts: (ctypes.c_void_p * k)(*[t.data_ptr() for t in ts])  # noqa: E731
+    st = bse.Status()
+    failed = ctypes.c_int64(0)
+    ns = np.zeros((k, n), dtype=np.int64)
+    nn = np.zeros(k, dtype=np.int64)
+    rc = bse._lib.lib().bse_solve_batched(
+        bse.default_context().handle, int(bse.Method.Chol), n, k, arr(ha), n, arr(hb), n, arr(hl),
+        arr(hv), 2 * n, ns.ctypes.data_as(ctypes.c_void_p), nn.ctypes.data_as(ctypes.c_void_p),
+        ctypes.byref(failed), ctypes.byref(st))
+    assert rc == 0, st.message
+    assert failed.value == -1
+    for i, h in enumerate(hs):
+        one = bse.solve_chol(h)
+        assert np.array_equal(hl[i].numpy(), one.lambda_)
+        assert np.array_equal(hv[i].numpy().T, one.v)
