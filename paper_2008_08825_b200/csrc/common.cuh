@@ -97,6 +97,28 @@ __device__ __forceinline__ void zcfma(z_t& acc, z_t a, z_t b) {
 __device__ __forceinline__ double zabs2(z_t a) { return a.x * a.x + a.y * a.y; }
 
 // ------------------------------------------------------------------ warp/block reductions
+// Grid-wide barrier for cooperative (co-resident) launches: after a CTA barrier, thread 0
+// adds 1 to a per-launch zeroed counter with a release reduction (no round trip) and polls
+// it with acquire loads until every CTA of this epoch has arrived; the closing CTA barrier
+// releases the block. One L2 round trip less than an arrive-with-return barrier.
+struct GridBarrier {
+  unsigned* ctr;
+  unsigned target;
+  __device__ __forceinline__ explicit GridBarrier(unsigned* c) : ctr(c), target(0) {}
+  __device__ __forceinline__ void sync() {
+    target += gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+  }
+};
+
 // Every warp-collective helper starts with warp_converge(): a warp that reaches a full-mask
 // shuffle in a diverged state (after lane-dependent branches) otherwise takes the BRA.DIV
 // fallback path, measured at ~14k cycles for a handful of shuffles in the panel kernels.

@@ -64,6 +64,7 @@ struct alignas(64) GebrdArgs {
   int64_t p0;
   int nbp, nch;
   unsigned long long* trace;  // optional per-phase timestamps (BSE_GEBRD_TRACE)
+  unsigned* bar;              // grid barrier counter, zeroed before every launch
   CUtensorMap tmap;           // TMA view of A (tile_ring.cuh)
 };
 
@@ -217,7 +218,7 @@ __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const i
 }
 
 __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_constant__ GebrdArgs a) {
-  cg::grid_group grid = cg::this_grid();
+  GridBarrier grid(a.bar);
   extern __shared__ __align__(16) unsigned char sm[];
   Ring ring;
   unsigned char* const sm_ring = sm + ((128u - (smem_u32(sm) & 127u)) & 127u);  // TMA alignment
@@ -571,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
 size_t gebrd_workspace_bytes(int64_t n) {
   const int64_t nch = ceil_div(n, kT);
   size_t z = 0;
-  z += size_t(n) * 2 * kNB * 2;     // VX, YU
+  z += 4 + size_t(n) * 2 * kNB * 2; // barrier counter, VX, YU
   z += size_t(n);                   // wrow
   z += size_t(nch) * nch * kT;      // P
   z += size_t(nch) * 2 * kNB;       // s12
@@ -588,6 +589,7 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   GebrdArgs a{};
   a.A = A; a.lda = lda; a.n = n; a.d = d; a.e = e; a.tauq = tauq; a.taup = taup;
   a.tmap = make_tile_map(A, lda, n);
+  a.bar = reinterpret_cast<unsigned*>(base); base += 4;  // 64 bytes, zeroed with VX / YU
   a.VX = base; base += n * 2 * kNB;
   a.YU = base; base += n * 2 * kNB;
   a.wrow = base; base += n;
@@ -616,7 +618,7 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   if (trace_path) BSE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), trace_n * 8, s));
   for (int64_t p0 = 0; p0 < n; p0 += kNB) {
     const int nbp = int(min64(kNB, n - p0));
-    BSE_CUDA(cudaMemsetAsync(a.VX, 0, sizeof(z_t) * size_t(n) * 2 * kNB * 2, s));
+    BSE_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(z_t) * (4 + size_t(n) * 2 * kNB * 2), s));
     a.p0 = p0;
     a.nbp = nbp;
     const int64_t m = n - p0;

@@ -55,6 +55,7 @@ struct alignas(64) HetrdArgs {
   z_t* s12p;      // nch x 2NB: per-slab partial W^H x | V^H x
   z_t* t12;       // 2NB : t1 = W^H v | t2 = V^H v
   double* vav;    // gridDim.x : per-CTA partials of v^H A22 v
+  unsigned* bar;  // grid barrier counter, zeroed before every launch
   unsigned long long* trace;  // optional per-phase timestamps (BSE_HETRD_TRACE)
   CUtensorMap tmap;           // TMA view of A (tile_ring.cuh)
   int64_t p0;
@@ -131,7 +132,7 @@ __device__ __forceinline__ void tri_coords(int64_t t, int& bi, int& bj) {
 // diagonal tile (never written, may hold garbage) is excluded by selects.
 __global__ void __launch_bounds__(kThreads, 1)
     hetrd_panel_kernel(const __grid_constant__ HetrdArgs a) {
-  cg::grid_group grid = cg::this_grid();
+  GridBarrier grid(a.bar);
   extern __shared__ __align__(16) unsigned char sm[];
   unsigned char* const sm_ring = sm + ((128u - (smem_u32(sm) & 127u)) & 127u);  // TMA alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_ring + sizeof(z_t) * kRing * kRingT * kRingT);
@@ -533,7 +534,7 @@ __global__ void set_last_diag_kernel(const z_t* A, int64_t lda, int64_t n, doubl
 size_t hetrd_workspace_bytes(int64_t n) {
   const int64_t nch = ceil_div(n, kT);
   size_t z = 0;
-  z += size_t(n) * 2 * NB * 2;  // VW, WV
+  z += 4 + size_t(n) * 2 * NB * 2;  // barrier counter, VW, WV
   z += size_t(nch) * nch * kT;  // Y
   z += size_t(nch) * 2 * NB;    // s12p
   z += size_t(2 * NB);          // t12
@@ -549,6 +550,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   a.A = A; a.lda = lda; a.n = n; a.d = d; a.e = e; a.tau = tau;
   a.tmap = make_tile_map(A, lda, n);
   a.ldp = n;
+  a.bar = reinterpret_cast<unsigned*>(base); base += 4;  // 64 bytes, zeroed with VW / WV
   a.VW = base; base += n * 2 * NB;
   a.WV = base; base += n * 2 * NB;
   a.Y = base; base += int64_t(nch) * nch * kT;
@@ -584,7 +586,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   if (trace_path) BSE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.trace), trace_n * 8, s));
   for (int64_t p0 = 0; p0 < n - 1; p0 += NB) {
     const int nbp = int(min64(NB, n - 1 - p0));
-    BSE_CUDA(cudaMemsetAsync(a.VW, 0, sizeof(z_t) * size_t(n) * 2 * NB * 2, s));
+    BSE_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(z_t) * (4 + size_t(n) * 2 * NB * 2), s));
     a.p0 = p0;
     a.nbp = nbp;
     // shrink the grid with the trailing size (fewer CTAs => cheaper grid barriers)
