@@ -445,4 +445,57 @@ void herm_dev_partials(cudaStream_t s, int64_t n, const z_t* M, int64_t ld, doub
   BSE_LAUNCH_CHECK();
 }
 
+// Diagonal of A scaled by `f` (E = lower(M1) with a halved diagonal for the X + X^H form of
+// the two-sided product).
+__global__ void scale_diag_kernel(int64_t n, z_t* A, int64_t lda, double f) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    A[i + i * lda] = zscale(A[i + i * lda], f);
+}
+
+void scale_diag(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double f) {
+  scale_diag_kernel<<<grid_for(n), 256, 0, s>>>(n, A, lda, f);
+  BSE_LAUNCH_CHECK();
+}
+
+// M(i,j) = X(i,j) + conj(X(j,i)) for i >= j (the lower triangle of X + X^H; the strict upper
+// triangle of M is not written). 32x32 tile pairs (I >= J): tile (J,I) is staged transposed
+// through shared memory so both reads are coalesced.
+__global__ void __launch_bounds__(256) herm_lower_sum_kernel(int64_t n, const z_t* __restrict__ X,
+                                                             int64_t ldx, z_t* __restrict__ M,
+                                                             int64_t ldm) {
+  __shared__ z_t t[32][33];
+  const int64_t nt = (n + 31) / 32;
+  // blockIdx.x enumerates the lower tile pairs (I >= J) row by row
+  const int64_t b = blockIdx.x;
+  int64_t I = int64_t((sqrt(8.0 * double(b) + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  while (I * (I + 1) / 2 > b) --I;
+  const int64_t J = b - I * (I + 1) / 2;
+  if (I >= nt) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // stage X(J-tile rows, I-tile cols) : element (J*32 + tx, I*32 + ty + 8k) -> t[ty+8k][tx]
+  for (int k = 0; k < 4; ++k) {
+    const int64_t r = J * 32 + tx, c = I * 32 + ty + 8 * k;
+    t[ty + 8 * k][tx] = (r < n && c < n) ? X[r + c * ldx] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int k = 0; k < 4; ++k) {
+    const int64_t i = I * 32 + tx, j = J * 32 + ty + 8 * k;
+    if (i < n && j < n && i >= j) {
+      // conj(X(j, i)) = conj(t[i - I*32][j - J*32])
+      const z_t xt = t[tx][ty + 8 * k];
+      const z_t x = X[i + j * ldx];
+      M[i + j * ldm] = make_double2(x.x + xt.x, x.y - xt.y);
+    }
+  }
+}
+
+void herm_lower_sum(cudaStream_t s, int64_t n, const z_t* X, int64_t ldx, z_t* M, int64_t ldm) {
+  if (n <= 0) return;
+  const int64_t nt = (n + 31) / 32;
+  herm_lower_sum_kernel<<<unsigned(nt * (nt + 1) / 2), 256, 0, s>>>(n, X, ldx, M, ldm);
+  BSE_LAUNCH_CHECK();
+}
+
 }  // namespace bseg

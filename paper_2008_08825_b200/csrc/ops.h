@@ -29,6 +29,10 @@ void tgk_refine(cudaStream_t s, int64_t n, const double* d, const double* e, dou
 void scale_cols_rsqrt(cudaStream_t s, int64_t rows, int64_t cols, z_t* X, int64_t ldx,
                       const double* lam);
 void square_vec(cudaStream_t s, int64_t n, const double* a, double* b);
+// A(i,i) *= f
+void scale_diag(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double f);
+// M(i,j) = X(i,j) + conj(X(j,i)) for i >= j (lower triangle of X + X^H)
+void herm_lower_sum(cudaStream_t s, int64_t n, const z_t* X, int64_t ldx, z_t* M, int64_t ldm);
 void reverse_real(cudaStream_t s, int64_t n, const double* a, double* b);
 void reverse_cols(cudaStream_t s, int64_t rows, int64_t cols, const z_t* a, int64_t lda, z_t* b,
                   int64_t ldb);

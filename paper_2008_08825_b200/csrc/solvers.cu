@@ -162,9 +162,14 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   clk.mark();
   certify(c, n, nullptr, b1, info);
   clk.mark();
-  // M = L^H M1 L  (solvers.cpp:122-123): T = L^H M1 -> b2 ; M = T L (lower half) -> b0
-  zgemm(s, 1, 0, n, n, n, kOne, b1, ld, b0, ld, kZero, b2, ld, kUpperOp, kGeneral, 0, nullptr, 0);
-  zgemm(s, 0, 0, n, n, n, kOne, b2, ld, b1, ld, kZero, b0, ld, kGeneral, kLowerOp, 1, nullptr, 0);
+  // M = L^H M1 L  (solvers.cpp:122-123), lower triangle only (zheevd reads 'L'), in the
+  // Hermitian form M = X + X^H with X = L^H (E L), E = lower(M1) with a halved diagonal:
+  // E L is lower x lower -> lower (n^3/6 complex MACs), L^H (E L) upper x lower (n^3/3),
+  // against n^3/2 + n^3/3 for (L^H M1) L.
+  scale_diag(s, n, b0, ld, 0.5);
+  zgemm(s, 0, 0, n, n, n, kOne, b0, ld, b1, ld, kZero, b2, ld, kLowerOp, kLowerOp, 1, nullptr, 0);
+  zgemm(s, 1, 0, n, n, n, kOne, b1, ld, b2, ld, kZero, b3, ld, kUpperOp, kLowerOp, 0, nullptr, 0);
+  herm_lower_sum(s, n, b3, ld, b0, ld);
   clk.mark();
   // hermitian_eig(M) (solvers.cpp:124 -> backend.cpp:34): hetrd + D&C + back-transform
   zhetrd_lower(s, n, b0, ld, d, e, tau, ws_hetrd);
