@@ -91,6 +91,24 @@ void certify(bse_ctx* c, int64_t n, z_t* F1, z_t* F2, int* info2) {
   (void)n;
 }
 
+// Certificate of M1 = A + B for CHOL, where the factor itself is not needed (the reference
+// factors it in product_pair, core.cpp:89-93, and discards it). M1 is congruent to
+// M = L^H M1 L, so M1 is positive definite iff every eigenvalue of M is positive: the
+// Cholesky of M1 only runs when the spectrum does not already certify it (or when M2 failed,
+// to report M1 first as the reference does). Throws NotDefinite{M1} like core.cpp:91-93.
+void certify_m1(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t* B, int64_t ldb,
+                z_t* m1, z_t* scratch, int* info0, z_t* ws) {
+  cudaStream_t s = c->stream;
+  zaddsub(s, n, A, lda, B, ldb, m1, scratch, n);
+  zpotrf_lower(s, n, m1, n, info0, ws, false);
+  int h = 0;
+  BSE_CUDA(cudaMemcpyAsync(&h, info0, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BSE_CUDA(cudaStreamSynchronize(s));
+  if (h != 0)
+    throw DomainError{BSE_ERR_NOT_DEFINITE, BSE_BLOCK_M1, int64_t(h) - 1,
+                      "A+B is not positive definite: " + pivot_msg(h)};
+}
+
 void read_flags(bse_ctx* c, int64_t n, const int64_t* d_counts, const int64_t* d_flagged,
                 std::vector<int64_t>& flagged, const char* what_if_bad) {
   int64_t cnt[3];
@@ -151,16 +169,21 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
 
   z_t* ws_potrf2 = w.take<z_t>(64 * 64);
   PhaseClock clk(c);
-  // product_pair: M1 -> b0, M2 -> b1 ; the certificate of M1 (on a copy, b2) and the
-  // factor L = chol(M2) (reused, solvers.cpp:121) run concurrently on two streams.
+  // product_pair: M1 -> b0, M2 -> b1 and the factor L = chol(M2) (reused, solvers.cpp:121).
+  // The certificate of M1 comes from the spectrum of M below (certify_m1).
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
-  fork(c);
-  zcopy2d(c->aux, n, n, b0, ld, b2, ld);
-  zpotrf_lower(c->aux, n, b2, ld, info + 0, ws_potrf2, false);
   zpotrf_lower(s, n, b1, ld, info + 1, ws_trsm, false);
-  join(c);
   clk.mark();
-  certify(c, n, nullptr, b1, info);
+  {
+    int h = 0;
+    BSE_CUDA(cudaMemcpyAsync(&h, info + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BSE_CUDA(cudaStreamSynchronize(s));
+    if (h != 0) {  // the reference certifies M1 first (core.cpp:89-99)
+      certify_m1(c, n, A, lda, B, ldb, b2, b3, info + 0, ws_potrf2);
+      throw DomainError{BSE_ERR_NOT_DEFINITE, BSE_BLOCK_M2, int64_t(h) - 1,
+                        "A-B is not positive definite: " + pivot_msg(h)};
+    }
+  }
   clk.mark();
   // M = L^H M1 L  (solvers.cpp:122-123), lower triangle only (zheevd reads 'L'), in the
   // Hermitian form M = X + X^H with X = L^H (E L), E = lower(M1) with a halved diagonal:
@@ -175,18 +198,23 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   zhetrd_lower(s, n, b0, ld, d, e, tau, ws_hetrd);
   clk.mark();
   dstedc(s, n, d, e, Z, ws_stedc, info + 2);
-  clk.mark();
-  real_to_complex(s, n, n, Z, n, b2, ld);
-  zunmtr_lower(s, n, b0, ld, tau, b2, ld, n, ws_unmtr);
-  clk.mark();
   {
     int h = 0;
+    double dmin = 0.0;
     BSE_CUDA(cudaMemcpyAsync(&h, info + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BSE_CUDA(cudaMemcpyAsync(&dmin, d, sizeof(double), cudaMemcpyDeviceToHost, s));
     BSE_CUDA(cudaStreamSynchronize(s));
+    // M1 is certified by the spectrum when its smallest eigenvalue is positive; otherwise
+    // factor it (b2, b3 are free here) and report NotDefinite{M1} as the reference would
+    if (h != 0 || !(dmin > 0.0)) certify_m1(c, n, A, lda, B, ldb, b3, b2, info + 0, ws_potrf2);
     if (h != 0)
       throw DomainError{BSE_ERR_CONVERGENCE_FAILURE, 0, -1,
                         "zheevd failed to converge (info=" + std::to_string(h) + ")"};
   }
+  clk.mark();
+  real_to_complex(s, n, n, Z, n, b2, ld);
+  zunmtr_lower(s, n, b0, ld, tau, b2, ld, n, ws_unmtr);
+  clk.mark();
   // lambda_from_squares (solvers.cpp:125)
   clamp_spectrum(s, n, d, 0, lam, flg, nonpos, counts, floor_p);
   // l1 = lambda^2 (after clamping), l2 = 1 for the assembly below

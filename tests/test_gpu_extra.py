@@ -344,3 +344,15 @@ def test_solve_batched_pinned_overlap():
         one = bse.solve_chol(h)
         assert np.array_equal(hl[i].numpy(), one.lambda_)
         assert np.array_equal(hv[i].numpy().T, one.v)
+
+
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+def test_both_blocks_indefinite_reports_m1(method):
+    """core.cpp:89-99 certifies M1 before M2; CHOL derives the M1 certificate from the
+    spectrum of L^H M1 L but must still report M1 first when both fail."""
+    n = 12
+    a = -np.eye(n, dtype=complex)
+    with pytest.raises(bse.NotDefinite) as e:
+        bse.solve(method, bse.from_blocks(a, np.zeros((n, n))))
+    assert e.value.which == bse.Block.M1
+    assert "leading minor of order 1 " in str(e.value)
