@@ -33,7 +33,9 @@ void ztrsm_lower(cudaStream_t s, int side, int op, int64_t n, int64_t other, con
 
 // Blocked Cholesky (lower) in place; *d_info receives LAPACK's info (0 ok, j+1 = first
 // failing pivot). Workspace: nb*nb complex. Strict upper left untouched unless zero_upper.
+// With s2 and ev[2]: look-ahead, the trailing update beyond the next block column runs on s2
+// (the factor is complete when s reaches the end of the enqueued work).
 void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z_t* ws,
-                  bool zero_upper);
+                  bool zero_upper, cudaStream_t s2 = nullptr, cudaEvent_t* ev = nullptr);
 
 }  // namespace bseg

@@ -219,6 +219,8 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
     BSE_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     BSE_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     BSE_CUDA(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+    for (auto& st2 : c->la) BSE_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    for (auto& ev : c->la_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : c->batch_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     // keep the stream-ordered staging buffers of bse_solve mapped between calls
     cudaMemPool_t pool;
@@ -258,6 +260,13 @@ int bse_ctx_destroy(bse_ctx* c) {
     cudaStreamDestroy(c->copy_in);
   }
   for (auto& ev : c->batch_ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& st2 : c->la)
+    if (st2) {
+      cudaStreamSynchronize(st2);
+      cudaStreamDestroy(st2);
+    }
+  for (auto& ev : c->la_ev)
     if (ev) cudaEventDestroy(ev);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);

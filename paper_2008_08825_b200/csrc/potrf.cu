@@ -216,7 +216,7 @@ __global__ void zero_strict_upper_kernel(int64_t n, z_t* A, int64_t lda) {
 }
 
 void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z_t* ws,
-                  bool zero_upper) {
+                  bool zero_upper, cudaStream_t s2, cudaEvent_t* ev) {
   (void)ws;  // kept for the call sites' workspace contract; the panel kernel needs none
   const size_t smem = size_t(kNB * kLD + 3 * kNB + kNB * (kPR + 1)) * sizeof(z_t) +
                       kNB * sizeof(double);
@@ -228,6 +228,11 @@ void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z
   }
   BSE_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), s));
   const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
+  // Look-ahead (with a second stream): the rank-jb update is split into the next block
+  // column (on s, so the next panel can start) and the rest of the trailing matrix (on s2,
+  // overlapping that panel). ev[0]: panel j done; ev[1]: the s2 update of step j-1 done.
+  const bool la = s2 != nullptr && ev != nullptr;
+  bool big_pending = false;
   for (int64_t j = 0; j < n; j += kNB) {
     const int jb = int(min64(kNB, n - j));
     z_t* Ajj = A + j + j * lda;
@@ -236,12 +241,30 @@ void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z
     zpotrf_panel_kernel<<<grid, 256, smem, s>>>(Ajj, lda, jb, j, rest, d_info);
     BSE_LAUNCH_CHECK();
     if (rest <= 0) break;
-    // HERK update A22 <- A22 - A21 A21^H (lower tiles only)
     z_t* A21 = A + (j + jb) + j * lda;
     z_t* A22 = A + (j + jb) + (j + jb) * lda;
-    zgemm(s, 0, 1, rest, rest, jb, mone, A21, lda, A21, lda, one, A22, lda, kGeneral, kGeneral, 1,
+    if (!la) {
+      // HERK update A22 <- A22 - A21 A21^H (lower tiles only)
+      zgemm(s, 0, 1, rest, rest, jb, mone, A21, lda, A21, lda, one, A22, lda, kGeneral, kGeneral,
+            1, nullptr, 0);
+      continue;
+    }
+    const int64_t jb2 = min64(kNB, rest), n2 = rest - jb2;
+    BSE_CUDA(cudaEventRecord(ev[0], s));
+    // next block column (rows >= j+jb): ordered after the s2 update of step j-1, which
+    // wrote the same columns
+    if (big_pending) BSE_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
+    zgemm(s, 0, 1, rest, jb2, jb, mone, A21, lda, A21, lda, one, A22, lda, kGeneral, kGeneral, 1,
           nullptr, 0);
+    if (n2 > 0) {
+      BSE_CUDA(cudaStreamWaitEvent(s2, ev[0], 0));
+      zgemm(s2, 0, 1, n2, n2, jb, mone, A21 + jb2, lda, A21 + jb2, lda, one,
+            A22 + jb2 + jb2 * lda, lda, kGeneral, kGeneral, 1, nullptr, 0);
+      BSE_CUDA(cudaEventRecord(ev[1], s2));
+      big_pending = true;
+    }
   }
+  if (la && big_pending) BSE_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
   if (zero_upper && n > 1) {
     const int blocks = int(min64(ceil_div(n * n, 256), 148 * 32));
     zero_strict_upper_kernel<<<blocks, 256, 0, s>>>(n, A, lda);

@@ -172,7 +172,7 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   // product_pair: M1 -> b0, M2 -> b1 and the factor L = chol(M2) (reused, solvers.cpp:121).
   // The certificate of M1 comes from the spectrum of M below (certify_m1).
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
-  zpotrf_lower(s, n, b1, ld, info + 1, ws_trsm, false);
+  zpotrf_lower(s, n, b1, ld, info + 1, ws_trsm, false, c->la[0], c->la_ev);
   clk.mark();
   {
     int h = 0;
@@ -286,8 +286,8 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   // product_pair + L1 = chol(M1), L2 = chol(M2) (solvers.cpp:138-140): b0 = L1, b1 = L2
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
   fork(c);
-  zpotrf_lower(c->aux, n, b0, ld, info + 0, ws_potrf2, false);
-  zpotrf_lower(s, n, b1, ld, info + 1, ws_potrf, false);
+  zpotrf_lower(c->aux, n, b0, ld, info + 0, ws_potrf2, false, c->la[0], c->la_ev);
+  zpotrf_lower(s, n, b1, ld, info + 1, ws_potrf, false, c->la[1], c->la_ev + 2);
   join(c);
   clk.mark();
   certify(c, n, b0, b1, info);
