@@ -103,6 +103,9 @@ __global__ void __launch_bounds__(256, 1)
       const z_t* cb = col + (c % 3) * kNB;
       if (warp != s) named_sync(1 + (c & 1));
       else __syncwarp();
+      // column c at this lane's rows, read once (the look-ahead pivot below writes another
+      // buffer, but the compiler cannot prove it and would reload per slot)
+      const z_t xc[2] = {cb[lane], cb[lane + 32]};
       // look-ahead: the owner of column c+1 (warp (s+1)&7, slot ps) updates and pivots it
       const int ps = (s == 7) ? 1 : 0;
       const bool ahead = (warp == ((s + 1) & 7)) && (c + 1 < kNB);
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int h = 0; h < 2; ++h) {
           const int r = lane + 32 * h;
           if ((h == 1 || k < 32) && r >= k) {
-            const z_t x = cb[r];
+            const z_t x = xc[h];
             z_t& v = reg[ps][h];
             v.x -= x.x * y.x + x.y * y.y;  // v -= x conj(y)
             v.y -= x.y * y.x - x.x * y.y;
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int h = 0; h < 2; ++h) {
             const int r = lane + 32 * h;
             if ((h == 1 || k < 32) && r >= k) {
-              const z_t x = cb[r];
+              const z_t x = xc[h];
               z_t& v = reg[j][h];
               v.x -= x.x * y.x + x.y * y.y;
               v.y -= x.y * y.x - x.x * y.y;
