@@ -55,8 +55,46 @@ void launch_z_short(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   BSE_LAUNCH_CHECK();
 }
 
+// Three-multiplication variant (gemm.cuh M3): the third accumulator set costs registers, so
+// the tile shrinks to 64x32 with 4 warps of 32x16 and 3 CTAs per SM.
+template <int BN, int BK, int ST, int MINB, bool CA, bool CB>
+void launch_z_3m_cfg(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
+  using T = ZGemmTile<kBM, BN, BK, kWM, kWNs, ST, CA, CB>;
+  auto kern = zgemm_dmma_kernel<kBM, BN, BK, kWM, kWNs, ST, CA, CB, MINB, true>;
+  static bool configured = false;
+  if (!configured) {
+    BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(T::SMEM)));
+    configured = true;
+  }
+  kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
+  BSE_LAUNCH_CHECK();
+}
+
+// 0: four-multiplication kernels only; 3 (default): the 3M 64x32 kernel for every complex
+// product; 5: 3M only for k > 128 (A/B switch BSE_GEMM_3M)
+int g3m_mode() {
+  static const int m = getenv("BSE_GEMM_3M") ? atoi(getenv("BSE_GEMM_3M")) : 3;
+  return m;
+}
+
+template <bool CA, bool CB>
+void launch_z_3m(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
+  // 64x32 tiles, 4 warps of 32x16, 3 CTAs per SM (measured 40-41 TFLOP/s complex-equivalent
+  // on 4096^3 against 33-35 for the four-multiplication 64x64 kernel)
+  const dim3 g2(grid.x, unsigned(ceil_div(p.n, 32)), grid.z);
+  launch_z_3m_cfg<32, 8, 4, 3, CA, CB>(s, p, g2);
+}
+
 void launch_z_any(cudaStream_t s, int opa, int opb, const ZGemmParams& p, dim3 grid) {
   static const bool no_short = getenv("BSE_GEMM_NO_SHORT") != nullptr;  // A/B switch
+  if (g3m_mode() == 3 || (g3m_mode() && p.k > 128)) {
+    if (!opa && !opb) launch_z_3m<false, false>(s, p, grid);
+    else if (!opa && opb) launch_z_3m<false, true>(s, p, grid);
+    else if (opa && !opb) launch_z_3m<true, false>(s, p, grid);
+    else launch_z_3m<true, true>(s, p, grid);
+    return;
+  }
   if (p.k <= 128 && p.ksplit == 1 && !no_short) {
     if (!opa && !opb) launch_z_short<false, false>(s, p, grid);
     else if (!opa && opb) launch_z_short<false, true>(s, p, grid);
@@ -123,12 +161,14 @@ void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_
   p.alpha = alpha; p.beta = beta;
   p.a_shape = a_shape; p.b_shape = b_shape; p.c_lower = c_lower;
   p.ksplit = 1;
-  const int64_t tiles_m = ceil_div(m, kBM), tiles_n = ceil_div(n, kBN);
+  // the 3M kernel runs 64x32 tiles, 3 resident CTAs per SM; the 4M kernels 64x64, 2 per SM
+  const bool m3 = g3m_mode() == 3 || (g3m_mode() && k > 128);
+  const int64_t tiles_m = ceil_div(m, kBM), tiles_n = ceil_div(n, m3 ? 32 : kBN);
   int ksplit = 1;
   // Under-filled grid with a long K: split K across CTAs (deterministic two-pass reduce).
-  // The split maximises the occupancy of the last wave (2 resident CTAs per SM), with a 1%
-  // per-slice penalty for the extra reduction traffic, and keeps >= 16 k-tiles per slice.
-  const int64_t tiles = tiles_m * tiles_n, slots = 2 * 148;
+  // The split maximises the occupancy of the last wave, with a 1% per-slice penalty for the
+  // extra reduction traffic, and keeps >= 16 k-tiles per slice.
+  const int64_t tiles = tiles_m * tiles_n, slots = (m3 ? 3 : 2) * 148;
   if (ws && tiles < slots && k >= 8 * kBK * 4) {
     double best = double(tiles) / double(slots);
     for (int ks = 2; ks <= 32 && int64_t(ks) * kBK * 16 <= k; ++ks) {
