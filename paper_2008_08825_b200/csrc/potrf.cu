@@ -6,6 +6,8 @@
 //      CTA 0 writes it back and reports the first non-positive / NaN pivot (LAPACK info),
 //      and each CTA solves its 32-row blocks of the panel A21 <- A21 L_jj^{-H} in place;
 //   2. HERK update A22 <- A22 - A21 * A21^H (lower)  (DMMA GEMM, lower tiles only)
+#include <cstdlib>
+
 #include "blas.h"
 #include "gemm.cuh"
 
@@ -41,7 +43,8 @@ __device__ __forceinline__ void named_arrive(int id) {
 //    finishes X(r,c) and shuffles it to the 7 others, which update their columns k > c. The
 //    CTA's first row block is fetched before the factorisation starts.
 __global__ void __launch_bounds__(256, 1)
-    zpotrf_panel_kernel(z_t* A, int64_t lda, int jb, int64_t j0, int64_t rest, int* info) {
+    zpotrf_panel_kernel(z_t* A, int64_t lda, int jb, int64_t j0, int64_t rest, int* info,
+                        unsigned* loaded) {
   extern __shared__ __align__(16) unsigned char sm[];
   z_t* Ls = reinterpret_cast<z_t*>(sm);  // factor, column-major, ld kLD
   z_t* col = Ls + kNB * kLD;             // 3 x 64 published columns
@@ -74,6 +77,16 @@ __global__ void __launch_bounds__(256, 1)
     }
   __syncthreads();
   if (failed) return;
+  // The factor is written back over the diagonal block the CTAs read: only the CTA that
+  // loads last (acq_rel count of loaded CTAs; CTAs of one launch need not be co-resident,
+  // e.g. behind a concurrent factorisation on another stream) may write it.
+  __shared__ int writer;
+  if (tid == 0) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(loaded) : "memory");
+    writer = (old == gridDim.x - 1) ? 1 : 0;
+  }
   // pivot + scale + publish of column c held in register slot `sl` of the owner warp
   auto pivot = [&](int c, z_t (&v)[2]) {
     warp_converge();
@@ -160,11 +173,13 @@ __global__ void __launch_bounds__(256, 1)
   }
   __syncthreads();
   if (failed) return;
-  if (blockIdx.x == 0)
+  if (writer) {
     for (int e = tid; e < jb * jb; e += blockDim.x) {
       const int i = e % jb, j = e / jb;
       A[i + int64_t(j) * lda] = Ls[i + j * kLD];
     }
+    if (tid == 0) *loaded = 0u;  // every CTA of this launch has counted; ready for the next
+  }
   // panel solve X L^H = B on kPR-row blocks of A21 = A + jb
   const int pr = tid >> 3, q = tid & 7;
   for (int64_t rb = blockIdx.x; rb * kPR < rest; rb += gridDim.x) {
@@ -220,7 +235,8 @@ __global__ void zero_strict_upper_kernel(int64_t n, z_t* A, int64_t lda) {
 
 void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z_t* ws,
                   bool zero_upper, cudaStream_t s2, cudaEvent_t* ev) {
-  (void)ws;  // kept for the call sites' workspace contract; the panel kernel needs none
+  // ws (>= 64 bytes, distinct per concurrent call) holds the panel kernel's loaded-CTA count
+  unsigned* loaded = reinterpret_cast<unsigned*>(ws);
   const size_t smem = size_t(kNB * kLD + 3 * kNB + kNB * (kPR + 1)) * sizeof(z_t) +
                       kNB * sizeof(double);
   static bool configured = false;
@@ -230,18 +246,20 @@ void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z
     configured = true;
   }
   BSE_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), s));
+  BSE_CUDA(cudaMemsetAsync(loaded, 0, sizeof(unsigned), s));
   const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
   // Look-ahead (with a second stream): the rank-jb update is split into the next block
   // column (on s, so the next panel can start) and the rest of the trailing matrix (on s2,
   // overlapping that panel). ev[0]: panel j done; ev[1]: the s2 update of step j-1 done.
-  const bool la = s2 != nullptr && ev != nullptr;
+  static const bool no_la = getenv("BSE_POTRF_NO_LA") != nullptr;  // A/B switch
+  const bool la = s2 != nullptr && ev != nullptr && !no_la;
   bool big_pending = false;
   for (int64_t j = 0; j < n; j += kNB) {
     const int jb = int(min64(kNB, n - j));
     z_t* Ajj = A + j + j * lda;
     const int64_t rest = n - j - jb;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(rest, kPR))));
-    zpotrf_panel_kernel<<<grid, 256, smem, s>>>(Ajj, lda, jb, j, rest, d_info);
+    zpotrf_panel_kernel<<<grid, 256, smem, s>>>(Ajj, lda, jb, j, rest, d_info, loaded);
     BSE_LAUNCH_CHECK();
     if (rest <= 0) break;
     z_t* A21 = A + (j + jb) + j * lda;

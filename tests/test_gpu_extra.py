@@ -356,3 +356,35 @@ def test_both_blocks_indefinite_reports_m1(method):
         bse.solve(method, bse.from_blocks(a, np.zeros((n, n))))
     assert e.value.which == bse.Block.M1
     assert "leading minor of order 1 " in str(e.value)
+
+
+# ------------------------------------------------------ large solves through device diagnostics
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+def test_large_solve_device_residual(method):
+    """n = 3072 through bse_solve_device, checked with the device residual.
+    Regression: CHOL+SVD factors A+B and A-B concurrently on two streams, so the CTAs of one
+    Cholesky panel launch need not be co-resident; the panel kernel must not overwrite the
+    diagonal block before its last CTA has read it (potrf.cu). Three repetitions because
+    that race depended on scheduling."""
+    import torch
+
+    n = 3072
+    a, b = configs.config2(0, n=n)
+    dev = torch.device("cuda", 0)
+    da = torch.from_numpy(a.T.copy()).to(dev)
+    db = torch.from_numpy(b.T.copy()).to(dev)
+    lam = torch.empty(n, dtype=torch.float64, device=dev)
+    v = torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)
+    res = torch.empty(n, dtype=torch.float64, device=dev)
+    ref = None
+    for _ in range(3):
+        flags = bse.solve_device(method, n, da.data_ptr(), db.data_ptr(), lam.data_ptr(),
+                                 v.data_ptr())
+        assert flags == []
+        bse.residual_device(n, da.data_ptr(), db.data_ptr(), n, lam.data_ptr(), v.data_ptr(),
+                            res.data_ptr())
+        assert res.max().item() <= 100 * n * EPS
+        got = lam.cpu().numpy()
+        if ref is None:
+            ref = got
+        assert np.array_equal(got, ref)  # bit-deterministic run to run
