@@ -132,7 +132,11 @@ const char* error_kind(const Error& e) {
   if (dynamic_cast<const ConvergenceFailure*>(&e)) return "ConvergenceFailure";
   if (dynamic_cast<const SingularFactor*>(&e)) return "SingularFactor";
   if (dynamic_cast<const NonPositiveScale*>(&e)) return "NonPositiveScale";
+  if (dynamic_cast<const OddDimension*>(&e)) return "OddDimension";
+  if (dynamic_cast<const LengthMismatch*>(&e)) return "LengthMismatch";
   if (dynamic_cast<const InvalidSpec*>(&e)) return "InvalidSpec";
+  if (dynamic_cast<const ParseError*>(&e)) return "ParseError";
+  if (dynamic_cast<const IoError*>(&e)) return "IoError";
   if (dynamic_cast<const DeviceError*>(&e)) return "DeviceError";
   return "Error";
 }
