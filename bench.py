@@ -165,6 +165,7 @@ def main():
     ap.add_argument("--method", default="chol", choices=["chol", "chol-svd"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lanes", type=int, default=2, help="matrices in flight per GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -181,8 +182,12 @@ def main():
     ctx.set_kernel_timing(True)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
 
-    # ---- inputs: W + K distinct matrices of this rank's shard, resident in HBM
-    total = args.warmup + args.steps
+    # ---- inputs: (W + K) x lanes distinct matrices of this rank's shard, resident in HBM.
+    # One step = `lanes` matrices in flight on this GPU (bse_solve_batched_device: item i on
+    # lane i % lanes, each lane's cooperative panel kernels on 1/lanes of the SMs).
+    lanes = max(1, args.lanes)
+    ctx.set_batch_lanes(lanes)
+    total = (args.warmup + args.steps) * lanes
     seeds = seeds_for(rank, world, total)
     host = []
     d_in = []
@@ -193,21 +198,18 @@ def main():
         host.append((ha, hb))
         d_in.append((ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)))
     torch.cuda.synchronize()
-    d_lam = torch.empty(n, dtype=torch.float64, device=dev)
-    d_v = torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)  # 2n x n column-major
-    lam_all = torch.empty((world, n), dtype=torch.float64, device=dev)
+    d_lams = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(total)]
+    d_vs = [torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)  # 2n x n col-major
+            for _ in range(lanes)]  # item i writes lane i % lanes's buffer (sequential per lane)
+    lam_all = torch.empty((world, args.steps * lanes, n), dtype=torch.float64, device=dev)
 
-    def step(i):
-        da, db = d_in[i]
-        bse.solve_device(meth, n, da.data_ptr(), db.data_ptr(), d_lam.data_ptr(), d_v.data_ptr(),
-                         ctx=ctx)
-        if world > 1:
-            import torch.distributed as dist
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(lam_all, d_lam)
+    def run_items(lo, hi):
+        bse.solve_batched_device(meth, n, [d_in[i][0].data_ptr() for i in range(lo, hi)],
+                                 [d_in[i][1].data_ptr() for i in range(lo, hi)],
+                                 [d_lams[i].data_ptr() for i in range(lo, hi)],
+                                 [d_vs[i % lanes].data_ptr() for i in range(lo, hi)], ctx=ctx)
 
-    for i in range(args.warmup):
-        step(i)
+    run_items(0, args.warmup * lanes)
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
@@ -215,23 +217,35 @@ def main():
     launches0 = ctx.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    phase_hist = []
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        for k in range(args.steps):
-            step(args.warmup + k)
-            phase_hist.append(ctx.phase_times())
+        run_items(args.warmup * lanes, total)
+        if world > 1:  # every matrix's eigenvalues to every rank
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(lam_all, torch.stack(d_lams[args.warmup * lanes:]))
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = ctx.kernel_launches() - launches0
+    phase_hist = [ctx.phase_times()]  # lane 0's last solve, with per-kernel event timings
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * flops(method, n) / (ms_per_step / 1e3) / 1e12
+    value = world * lanes * flops(method, n) / (ms_per_step / 1e3) / 1e12
+    # latency of one solve alone (whole GPU, no concurrent lane), for reference
+    torch.cuda.synchronize()
+    l0 = torch.cuda.Event(enable_timing=True)
+    l1 = torch.cuda.Event(enable_timing=True)
+    l0.record(stream)
+    for i in range(2):
+        bse.solve_device(meth, n, d_in[i][0].data_ptr(), d_in[i][1].data_ptr(),
+                         d_lams[i].data_ptr(), d_vs[0].data_ptr(), ctx=ctx)
+    l1.record(stream)
+    torch.cuda.synchronize()
+    single_ms = l0.elapsed_time(l1) / 2
 
     # ---- end to end through the host-pointer C-ABI: every step's inputs go H2D from pinned
     # host memory and its (lambda, V) come back D2H inside the timed region. Headline: the
@@ -244,11 +258,11 @@ def main():
         import ctypes
         L = bse._lib.lib()
         st = bse.Status()
-        nv = min(args.steps, 8)  # distinct pinned outputs (reused cyclically beyond 8 steps)
+        nv = min(args.steps * lanes, 8)  # distinct pinned outputs (reused cyclically beyond 8)
         hv = [torch.empty((n, 2 * n), dtype=torch.complex128).pin_memory() for _ in range(nv)]
         hl = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(nv)]
-        ns = np.zeros((max(args.steps, args.warmup), n), dtype=np.int64)
-        nn = np.zeros(max(args.steps, args.warmup), dtype=np.int64)
+        ns = np.zeros((total, n), dtype=np.int64)
+        nn = np.zeros(total, dtype=np.int64)
         failed = ctypes.c_int64(-1)
 
         def arr(ts):
@@ -293,20 +307,22 @@ def main():
                 ems = float(t.item())
             return ems
 
-        batched(host[: args.warmup])  # untimed: staging buffers, streams, first touches
-        ems = timed(lambda: batched(host[args.warmup: args.warmup + args.steps]))
+        batched(host[: args.warmup * lanes])  # untimed: staging buffers, lane contexts
+        ems = timed(lambda: batched(host[args.warmup * lanes: total]))
         for k in range(args.warmup):
             single(*host[k])
         ems1 = timed(lambda: [single(*host[args.warmup + k]) for k in range(args.steps)])
-        e2e = {"value": world * flops(method, n) / (ems / args.steps / 1e3) / 1e12,
-               "unit": "TFLOP/s", "h2d_bytes_per_step": 2 * n * n * 16,
-               "d2h_bytes_per_step": 2 * n * n * 16 + n * 8,
+        e2e = {"value": world * lanes * flops(method, n) / (ems / args.steps / 1e3) / 1e12,
+               "unit": "TFLOP/s", "h2d_bytes_per_step": lanes * 2 * n * n * 16,
+               "d2h_bytes_per_step": lanes * (2 * n * n * 16 + n * 8),
                "ms_per_step": ems / args.steps,
-               "path": "bse_solve_batched over the K timed matrices (pinned host buffers; "
-                       "upload of item i+1 and download of item i-1 overlap solve i)",
+               "path": f"bse_solve_batched over the K x {lanes} timed matrices ({lanes} lanes; "
+                       "pinned host buffers; each lane uploads its next item and downloads its "
+                       "previous one while it solves)",
                "single_call": {"value": world * flops(method, n) / (ems1 / args.steps / 1e3) / 1e12,
-                               "ms_per_step": ems1 / args.steps,
-                               "path": "one bse_solve per step (pinned; V streamed in chunks)"}}
+                               "ms_per_matrix": ems1 / args.steps,
+                               "path": "one bse_solve per matrix, one matrix at a time (pinned; "
+                                       "V streamed back in chunks)"}}
 
     # ---- roofline of the dominant kernel class from the live event timings
     peaks = load_peaks()
@@ -370,12 +386,14 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": f"config5: batch of 64 complex128 n={n} BSE matrices "
                                    f"(config-2 generator, seeds 0..63), {method}; each step every "
-                                   "GPU solves one matrix of its seed shard",
-                       "n": n, "method": method, "batch": 64, "matrices_per_step_per_gpu": 1,
+                                   f"GPU solves {lanes} matrices of its seed shard concurrently "
+                                   "(bse_solve_batched_device, one lane per matrix)",
+                       "n": n, "method": method, "batch": 64, "matrices_per_step_per_gpu": lanes,
                        "l2": "inputs 512 MiB per solve (> 126 MB L2), distinct per step",
                        "parallelism": f"dp{world} (seed partition, NCCL gathers eigenvalues)"},
-            "s_per_solve": ms_per_step / 1e3,
-            "batch64_s": ms_per_step / 1e3 * 64 / world,
+            "s_per_solve": ms_per_step / 1e3 / lanes,
+            "single_solve_latency_ms": single_ms,
+            "batch64_s": ms_per_step / 1e3 / lanes * 64 / world,
             "fp64_frac_of_peak": value / (world * fp64_peak),
             "phase_ms": {k: round(v, 3) for k, v in ph.items()
                          if k in ("product_pair", "triple", "reduce", "tridiag", "backtransform",

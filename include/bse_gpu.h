@@ -99,7 +99,7 @@ int bse_ctx_destroy(bse_ctx* ctx);
 void* bse_ctx_stream(bse_ctx* ctx);
 /* Per-phase timings of the most recent solve on this context (zeros before the first). */
 int bse_ctx_last_phase_times(bse_ctx* ctx, bse_phase_times* out);
-/* Number of kernels this library launched on the context since creation. */
+/* Number of kernels this library launched on the context (and its batch lanes) since creation. */
 int64_t bse_ctx_kernel_launches(bse_ctx* ctx);
 /* Enables CUDA-event timing of the panel and GEMM kernels (fills panel_ and gemm_ fields). */
 int bse_ctx_set_kernel_timing(bse_ctx* ctx, int enable);
@@ -134,7 +134,8 @@ int bse_solve_device(bse_ctx* ctx, int method, int64_t n,
 /* Batch driver: solves `batch` independent matrices with the same
  * method and shape from host buffers a[i], b[i] into lambda[i], v[i]. The upload of matrix
  * i+1 and the download of matrix i-1 run on copy streams while matrix i computes, so with
- * page-locked host buffers the PCIe traffic hides behind the solves.
+ * page-locked host buffers the PCIe traffic hides behind the solves. Items run on
+ * bse_ctx_set_batch_lanes() lanes (default 2 solves in flight, item i on lane i % lanes).
  *   near_singular  : null or capacity batch*n (row i holds matrix i's flagged indices)
  *   n_near_singular: null or capacity batch
  *   failed_index   : null or receives the first failing item (-1 when all succeed); the
@@ -144,6 +145,18 @@ int bse_solve_batched(bse_ctx* ctx, int method, int64_t n, int64_t batch,
                       double* const* lambda, double* const* v, int64_t ldv,
                       int64_t* near_singular, int64_t* n_near_singular, int64_t* failed_index,
                       bse_status* st);
+
+/* Same over device pointers (a[i], b[i], lambda[i], v[i] on the context's device), e.g. a
+ * batch already resident in HBM. Synchronous at return. */
+int bse_solve_batched_device(bse_ctx* ctx, int method, int64_t n, int64_t batch,
+                             const double* const* d_a, int64_t lda, const double* const* d_b,
+                             int64_t ldb, double* const* d_lambda, double* const* d_v,
+                             int64_t ldv, int64_t* near_singular, int64_t* n_near_singular,
+                             int64_t* failed_index, bse_status* st);
+/* Solves in flight per batch call, 1..4 (default 2). With L > 1 the batch runs on L contexts
+ * at once (L - 1 created on first use) and each cooperative panel kernel is limited to 1/L of
+ * the SMs, so one solve's latency-bound reductions overlap another's GEMM phases. */
+int bse_ctx_set_batch_lanes(bse_ctx* ctx, int lanes);
 
 /* ---------------------------------------------------------------- core glue (core.cpp) */
 /* product_pair (core.cpp:87-100): m1 = a+b, m2 = a-b, each certified by Cholesky.     */

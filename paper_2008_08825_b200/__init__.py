@@ -33,7 +33,7 @@ __all__ = [
     "ConvergenceFailure", "SingularFactor", "NonPositiveScale", "InvalidSpec", "DeviceError",
     "from_blocks", "product_pair", "assemble_eigenvectors", "solve_chol", "solve_chol_svd",
     "solve", "negative_spectrum", "hermitian_eig", "cholesky_lower", "svd", "tri_solve", "matmul",
-    "solve_sqrt", "solve_reference", "solve_batched", "BatchError", "hpd_sqrt", "residual", "sigma_orthogonality_error",
+    "solve_sqrt", "solve_reference", "solve_batched", "solve_batched_device", "BatchError", "hpd_sqrt", "residual", "sigma_orthogonality_error",
     "check_form1", "check_form2", "check_pairing", "predicted_error", "OddDimension",
     "residual_device", "sigma_orthogonality_error_device",
     "LengthMismatch",
@@ -258,6 +258,11 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(_lib.lib().bse_ctx_kernel_launches(self._h))
+
+    def set_batch_lanes(self, lanes: int):
+        """Solves in flight per batch call (1..4, default 2), see bse_ctx_set_batch_lanes."""
+        if _lib.lib().bse_ctx_set_batch_lanes(self._h, int(lanes)) != 0:
+            raise InvalidSpec("batch lanes must be 1..4")
 
     def stream(self) -> int:
         return int(_lib.lib().bse_ctx_stream(self._h) or 0)
@@ -574,6 +579,28 @@ def solve_device(method: Method, n: int, a_ptr: int, b_ptr: int, lam_ptr: int, v
                                      ldv or 2 * n, _p(ns), ctypes.byref(nn), ctypes.byref(st))
     _check(rc, st)
     return [int(i) for i in ns[: nn.value]]
+
+
+def solve_batched_device(method: Method, n: int, a_ptrs: List[int], b_ptrs: List[int],
+                         lam_ptrs: List[int], v_ptrs: List[int],
+                         ctx: Optional[Context] = None) -> List[List[int]]:
+    """bse_solve_batched_device: a batch resident in device memory (column-major a, b with
+    ld n; lambda n; v 2n x n with ld 2n). Returns each item's near-singular indices."""
+    ctx = ctx or default_context()
+    k = len(a_ptrs)
+    if not (len(b_ptrs) == len(lam_ptrs) == len(v_ptrs) == k):
+        raise LengthMismatch("solve_batched_device: pointer lists differ in length")
+    arr = lambda xs: (ctypes.c_void_p * max(k, 1))(*xs)  # noqa: E731
+    ns = np.zeros((max(k, 1), max(n, 1)), dtype=np.int64)
+    nn = np.zeros(max(k, 1), dtype=np.int64)
+    failed = ctypes.c_int64(-1)
+    st = Status()
+    rc = _lib.lib().bse_solve_batched_device(ctx.handle, int(method), n, k, arr(a_ptrs), n,
+                                             arr(b_ptrs), n, arr(lam_ptrs), arr(v_ptrs), 2 * n,
+                                             _p(ns), _p(nn), ctypes.byref(failed),
+                                             ctypes.byref(st))
+    _check(rc, st)
+    return [[int(j) for j in ns[i, : nn[i]]] for i in range(k)]
 
 
 # --------------------------------------------------------------------------- backend (backend.cpp)

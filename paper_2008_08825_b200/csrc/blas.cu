@@ -17,6 +17,7 @@ namespace bseg {
 
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local KernelTimer* g_timer = nullptr;
+thread_local int g_panel_ctas = 0;
 
 namespace {
 

@@ -4,6 +4,9 @@
 // solvers.hpp, types.hpp) onto plain pointers + status codes. Host-pointer entry points
 // stage through the context's device arena; nothing here ever computes on the CPU: when
 // no CUDA device is present every compute entry point fails with BSE_ERR_NO_DEVICE.
+#include <atomic>
+#include <climits>
+#include <thread>
 #include <cfloat>
 #include <cstring>
 #include <string>
@@ -239,6 +242,8 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
 
 int bse_ctx_destroy(bse_ctx* c) {
   if (!c) return BSE_OK;
+  for (auto& t : c->twin)
+    if (t) bse_ctx_destroy(t);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->arena) cudaFree(c->arena);
@@ -283,7 +288,12 @@ int bse_ctx_last_phase_times(bse_ctx* c, bse_phase_times* out) {
   return BSE_OK;
 }
 
-int64_t bse_ctx_kernel_launches(bse_ctx* c) { return c ? c->launches : 0; }
+int64_t bse_ctx_kernel_launches(bse_ctx* c) {  // including the batch lanes' contexts
+  if (!c) return 0;
+  int64_t total = c->launches;
+  for (bse_ctx* t : c->twin) total += t ? t->launches : 0;
+  return total;
+}
 
 int bse_ctx_set_kernel_timing(bse_ctx* c, int enable) {
   if (!c) return BSE_ERR_INVALID_SPEC;
@@ -358,87 +368,240 @@ int bse_solve(bse_ctx* c, int method, int64_t n, const double* a, int64_t lda, c
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Items of one batch lane: every item index i with i % lanes == lane, in order.
+std::vector<int64_t> lane_items(int64_t batch, int lanes, int lane) {
+  std::vector<int64_t> v;
+  for (int64_t i = lane; i < batch; i += lanes) v.push_back(i);
+  return v;
+}
+
+struct BatchIO {  // the caller's per-item arrays (host or device pointers)
+  int method;
+  int64_t n, lda, ldb, ldv;
+  const double* const* a;
+  const double* const* b;
+  double* const* lambda;
+  double* const* v;
+  int64_t* near_singular;
+  int64_t* n_near_singular;
+  bool device;  // a, b, lambda, v are device pointers (bse_solve_batched_device)
+};
+
+// First failing item over all lanes: later items of every lane are skipped once it is known.
+struct BatchFail {
+  std::mutex mu;
+  std::atomic<int64_t> first{INT64_MAX};
+  bool domain = false;
+  DomainError err{};
+  std::exception_ptr other;
+  void record(int64_t i, const DomainError* d, std::exception_ptr e) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (i >= first.load()) return;
+    first = i;
+    domain = d != nullptr;
+    if (d) err = *d;
+    other = d ? nullptr : e;
+  }
+};
+
+void store_flags(const BatchIO& io, int64_t i, const std::vector<int64_t>& flagged) {
+  if (io.n_near_singular) io.n_near_singular[i] = int64_t(flagged.size());
+  if (io.near_singular)
+    for (size_t f = 0; f < flagged.size(); ++f) io.near_singular[i * io.n + int64_t(f)] = flagged[f];
+}
+
+// One lane on context c. Host pointers: two slots of (A, B, V, lambda) staging, item j+1
+// uploads on c->copy_in and item j-1 downloads on c->copy while item j computes on c->stream.
+// Device pointers: the items are solved in place, one after the other.
+void run_lane(bse_ctx* c, const BatchIO& io, const std::vector<int64_t>& items, BatchFail& fail) {
+  const int64_t n = io.n;
+  auto solve_item = [&](int64_t i, const z_t* A, int64_t lda, const z_t* B, int64_t ldb,
+                        double* L, z_t* V, int64_t ldv) -> bool {
+    std::vector<int64_t> flagged;
+    if (c->timing) c->timer.used = 0;
+    try {
+      run_solve(c, io.method, n, A, lda, B, ldb, L, V, ldv, flagged);
+    } catch (DomainError& e) {
+      e.msg = "batch item " + std::to_string(i) + ": " + e.msg;
+      fail.record(i, &e, nullptr);
+      return false;
+    }
+    collect_timer(c);
+    store_flags(io, i, flagged);
+    return true;
+  };
+  if (io.device) {
+    for (int64_t i : items) {
+      if (i > fail.first.load()) break;
+      if (!solve_item(i, reinterpret_cast<const z_t*>(io.a[i]), io.lda,
+                      reinterpret_cast<const z_t*>(io.b[i]), io.ldb, io.lambda[i],
+                      reinterpret_cast<z_t*>(io.v[i]), io.ldv))
+        break;
+    }
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  const size_t nn = size_t(n) * size_t(n);
+  const size_t slot = 2 * nn + 2 * nn + size_t(n) / 2 + 64;  // in z_t units
+  DevBuf buf(2 * slot * sizeof(z_t), c->stream);
+  z_t *dA[2], *dB[2], *dV[2];
+  double* dL[2];
+  for (int k = 0; k < 2; ++k) {
+    z_t* base = buf.as<z_t>() + k * slot;
+    dA[k] = base;
+    dB[k] = base + nn;
+    dV[k] = base + 2 * nn;
+    dL[k] = reinterpret_cast<double*>(base + 4 * nn);
+  }
+  struct Drain {  // the copy streams finish before the staging buffers are released
+    bse_ctx* c;
+    ~Drain() {
+      cudaStreamSynchronize(c->copy_in);
+      cudaStreamSynchronize(c->copy);
+    }
+  } drain{c};
+  cudaEvent_t* in_ready = c->batch_ev;       // [2] copy_in -> compute
+  cudaEvent_t* comp_done = c->batch_ev + 2;  // [2] compute -> copy_in / copy
+  cudaEvent_t* out_done = c->batch_ev + 4;   // [2] copy -> compute (slot reuse)
+  auto upload = [&](size_t j) {
+    const int k = int(j & 1);
+    const int64_t i = items[j];
+    if (j >= 2) BSE_CUDA(cudaStreamWaitEvent(c->copy_in, comp_done[k], 0));
+    BSE_CUDA(cudaMemcpy2DAsync(dA[k], size_t(n) * sizeof(z_t), io.a[i], size_t(io.lda) * sizeof(z_t),
+                               size_t(n) * sizeof(z_t), size_t(n), cudaMemcpyHostToDevice,
+                               c->copy_in));
+    BSE_CUDA(cudaMemcpy2DAsync(dB[k], size_t(n) * sizeof(z_t), io.b[i], size_t(io.ldb) * sizeof(z_t),
+                               size_t(n) * sizeof(z_t), size_t(n), cudaMemcpyHostToDevice,
+                               c->copy_in));
+    BSE_CUDA(cudaEventRecord(in_ready[k], c->copy_in));
+  };
+  // the staging allocation is ordered on c->stream; the copy-in stream starts after it
+  BSE_CUDA(cudaEventRecord(c->batch_ev[6], c->stream));
+  BSE_CUDA(cudaStreamWaitEvent(c->copy_in, c->batch_ev[6], 0));
+  if (!items.empty()) upload(0);
+  for (size_t j = 0; j < items.size(); ++j) {
+    const int64_t i = items[j];
+    if (i > fail.first.load()) break;
+    const int k = int(j & 1);
+    if (j + 1 < items.size()) upload(j + 1);
+    BSE_CUDA(cudaStreamWaitEvent(c->stream, in_ready[k], 0));
+    if (j >= 2) BSE_CUDA(cudaStreamWaitEvent(c->stream, out_done[k], 0));
+    if (!solve_item(i, dA[k], n, dB[k], n, dL[k], dV[k], 2 * n)) break;
+    BSE_CUDA(cudaEventRecord(comp_done[k], c->stream));
+    BSE_CUDA(cudaStreamWaitEvent(c->copy, comp_done[k], 0));
+    BSE_CUDA(cudaMemcpyAsync(io.lambda[i], dL[k], sizeof(double) * size_t(n),
+                             cudaMemcpyDeviceToHost, c->copy));
+    BSE_CUDA(cudaMemcpy2DAsync(io.v[i], size_t(io.ldv) * sizeof(z_t), dV[k],
+                               size_t(2 * n) * sizeof(z_t), size_t(2 * n) * sizeof(z_t),
+                               size_t(n), cudaMemcpyDeviceToHost, c->copy));
+    BSE_CUDA(cudaEventRecord(out_done[k], c->copy));
+  }
+  BSE_CUDA(cudaStreamSynchronize(c->copy));
+  BSE_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// The batch on `lanes` contexts at once (c and its lazily created twins), one host thread
+// per extra lane; each lane's cooperative panel kernels get 1/lanes of the SMs, so one lane's
+// latency-bound tridiagonal / bidiagonal reductions overlap another lane's GEMM phases.
+void run_batch(bse_ctx* c, const BatchIO& io, int64_t batch, int64_t* failed_index) {
+  if (failed_index) *failed_index = -1;
+  if (batch == 0) return;
+  const int lanes = int(std::min<int64_t>(c->batch_lanes, batch));
+  int sms = 0;
+  BSE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const int prev_cap = g_panel_ctas;
+  g_panel_ctas = lanes > 1 ? sms / lanes : 0;
+  struct Restore {
+    int v;
+    ~Restore() { g_panel_ctas = v; }
+  } restore{prev_cap};
+  BatchFail fail;
+  std::vector<std::thread> extra;
+  std::vector<std::exception_ptr> lane_err(static_cast<size_t>(lanes));
+  for (int l = 1; l < lanes; ++l) {
+    if (!c->twin[l - 1]) {
+      bse_status st{};
+      if (bse_ctx_create(&c->twin[l - 1], c->device, &st) != BSE_OK)
+        throw std::runtime_error(std::string("batch lane context: ") + st.message);
+    }
+    bse_ctx* lc = c->twin[l - 1];
+    const int cap = g_panel_ctas;
+    extra.emplace_back([&, l, lc, cap] {
+      try {
+        BSE_CUDA(cudaSetDevice(lc->device));
+        g_launch_counter = &lc->launches;
+        g_timer = nullptr;
+        g_panel_ctas = cap;
+        run_lane(lc, io, lane_items(batch, lanes, l), fail);
+      } catch (...) {
+        lane_err[size_t(l)] = std::current_exception();
+      }
+    });
+  }
+  try {
+    run_lane(c, io, lane_items(batch, lanes, 0), fail);
+  } catch (...) {
+    lane_err[0] = std::current_exception();
+  }
+  for (auto& t : extra) t.join();
+  for (auto& e : lane_err)
+    if (e) std::rethrow_exception(e);  // CUDA / allocation failure of a lane
+  if (fail.first.load() != INT64_MAX) {
+    if (failed_index) *failed_index = fail.first.load();
+    if (fail.domain) throw fail.err;
+    std::rethrow_exception(fail.other);
+  }
+}
+
+void check_batch(int64_t n, int64_t lda, int64_t ldb, int64_t ldv, int64_t batch,
+                 const void* a, const void* b, const void* l, const void* v) {
+  check_dims(n, lda, ldb);
+  if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
+  if (batch < 0) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "negative batch"};
+  if (batch > 0 && (!a || !b || !l || !v))
+    throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "null batch pointer array"};
+}
+
+}  // namespace
+
+extern "C" {
+
 int bse_solve_batched(bse_ctx* c, int method, int64_t n, int64_t batch, const double* const* a,
                       int64_t lda, const double* const* b, int64_t ldb, double* const* lambda,
                       double* const* v, int64_t ldv, int64_t* near_singular,
                       int64_t* n_near_singular, int64_t* failed_index, bse_status* st) {
   if (failed_index) *failed_index = -1;
   return guarded(c, st, [&] {
-    check_dims(n, lda, ldb);
-    if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
-    if (batch < 0) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "negative batch"};
-    if (batch == 0) return;
-    if (!a || !b || !lambda || !v)
-      throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "null batch pointer array"};
-    const size_t nn = size_t(n) * size_t(n);
-    // two slots of (A, B, V, lambda): matrix i+1 uploads and matrix i-1 downloads while
-    // matrix i computes (copy-in on c->copy_in, copy-out on c->copy, compute on c->stream)
-    const size_t slot = 2 * nn + 2 * nn + size_t(n) / 2 + 64;  // in z_t units
-    DevBuf buf(2 * slot * sizeof(z_t), c->stream);
-    z_t *dA[2], *dB[2], *dV[2];
-    double* dL[2];
-    for (int k = 0; k < 2; ++k) {
-      z_t* base = buf.as<z_t>() + k * slot;
-      dA[k] = base;
-      dB[k] = base + nn;
-      dV[k] = base + 2 * nn;
-      dL[k] = reinterpret_cast<double*>(base + 4 * nn);
-    }
-    struct Drain {  // the copy streams finish before the staging buffers are released
-      bse_ctx* c;
-      ~Drain() {
-        cudaStreamSynchronize(c->copy_in);
-        cudaStreamSynchronize(c->copy);
-      }
-    } drain{c};
-    cudaEvent_t* in_ready = c->batch_ev;       // [2] copy_in -> compute
-    cudaEvent_t* comp_done = c->batch_ev + 2;  // [2] compute -> copy_in / copy
-    cudaEvent_t* out_done = c->batch_ev + 4;   // [2] copy -> compute (slot reuse)
-    auto upload = [&](int64_t i) {
-      const int k = int(i & 1);
-      if (i >= 2) BSE_CUDA(cudaStreamWaitEvent(c->copy_in, comp_done[k], 0));
-      BSE_CUDA(cudaMemcpy2DAsync(dA[k], size_t(n) * sizeof(z_t), a[i], size_t(lda) * sizeof(z_t),
-                                 size_t(n) * sizeof(z_t), size_t(n), cudaMemcpyHostToDevice,
-                                 c->copy_in));
-      BSE_CUDA(cudaMemcpy2DAsync(dB[k], size_t(n) * sizeof(z_t), b[i], size_t(ldb) * sizeof(z_t),
-                                 size_t(n) * sizeof(z_t), size_t(n), cudaMemcpyHostToDevice,
-                                 c->copy_in));
-      BSE_CUDA(cudaEventRecord(in_ready[k], c->copy_in));
-    };
-    // the staging allocation is ordered on c->stream; the copy-in stream starts after it
-    BSE_CUDA(cudaEventRecord(c->batch_ev[6], c->stream));
-    BSE_CUDA(cudaStreamWaitEvent(c->copy_in, c->batch_ev[6], 0));
-    upload(0);
-    for (int64_t i = 0; i < batch; ++i) {
-      const int k = int(i & 1);
-      if (i + 1 < batch) upload(i + 1);
-      BSE_CUDA(cudaStreamWaitEvent(c->stream, in_ready[k], 0));
-      if (i >= 2) BSE_CUDA(cudaStreamWaitEvent(c->stream, out_done[k], 0));
-      std::vector<int64_t> flagged;
-      if (c->timing) c->timer.used = 0;
-      try {
-        run_solve(c, method, n, dA[k], n, dB[k], n, dL[k], dV[k], 2 * n, flagged);
-      } catch (DomainError& e) {
-        if (failed_index) *failed_index = i;
-        e.msg = "batch item " + std::to_string(i) + ": " + e.msg;
-        throw;
-      }
-      collect_timer(c);
-      BSE_CUDA(cudaEventRecord(comp_done[k], c->stream));
-      BSE_CUDA(cudaStreamWaitEvent(c->copy, comp_done[k], 0));
-      BSE_CUDA(cudaMemcpyAsync(lambda[i], dL[k], sizeof(double) * size_t(n),
-                               cudaMemcpyDeviceToHost, c->copy));
-      BSE_CUDA(cudaMemcpy2DAsync(v[i], size_t(ldv) * sizeof(z_t), dV[k],
-                                 size_t(2 * n) * sizeof(z_t), size_t(2 * n) * sizeof(z_t),
-                                 size_t(n), cudaMemcpyDeviceToHost, c->copy));
-      BSE_CUDA(cudaEventRecord(out_done[k], c->copy));
-      if (n_near_singular) n_near_singular[i] = int64_t(flagged.size());
-      if (near_singular)
-        for (size_t f = 0; f < flagged.size(); ++f) near_singular[i * n + int64_t(f)] = flagged[f];
-    }
-    BSE_CUDA(cudaStreamSynchronize(c->copy));
-    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    check_batch(n, lda, ldb, ldv, batch, a, b, lambda, v);
+    const BatchIO io{method, n, lda, ldb, ldv, a, b, lambda, v, near_singular, n_near_singular,
+                     false};
+    run_batch(c, io, batch, failed_index);
   });
+}
+
+int bse_solve_batched_device(bse_ctx* c, int method, int64_t n, int64_t batch,
+                             const double* const* d_a, int64_t lda, const double* const* d_b,
+                             int64_t ldb, double* const* d_lambda, double* const* d_v,
+                             int64_t ldv, int64_t* near_singular, int64_t* n_near_singular,
+                             int64_t* failed_index, bse_status* st) {
+  if (failed_index) *failed_index = -1;
+  return guarded(c, st, [&] {
+    check_batch(n, lda, ldb, ldv, batch, d_a, d_b, d_lambda, d_v);
+    const BatchIO io{method, n, lda, ldb, ldv, d_a, d_b, d_lambda, d_v, near_singular,
+                     n_near_singular, true};
+    run_batch(c, io, batch, failed_index);
+  });
+}
+
+int bse_ctx_set_batch_lanes(bse_ctx* c, int lanes) {
+  if (!c || lanes < 1 || lanes > 4) return BSE_ERR_INVALID_SPEC;
+  std::lock_guard<std::mutex> lock(c->mu);
+  c->batch_lanes = lanes;
+  return BSE_OK;
 }
 
 int bse_product_pair(bse_ctx* c, int64_t n, const double* a, int64_t lda, const double* b,

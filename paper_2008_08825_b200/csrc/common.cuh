@@ -48,6 +48,10 @@ struct KernelTimer {
   double work[4096];  // flops (GEMM) or algorithmic bytes (panel) of each timed launch
 };
 extern thread_local KernelTimer* g_timer;
+// Cap on the CTAs of the cooperative panel kernels (0 = every SM): the batch driver runs two
+// solves at once, each panel kernel on half of the SMs, so one solve's latency-bound panels
+// overlap the other's GEMM phases (set per calling thread from its context).
+extern thread_local int g_panel_ctas;
 inline int timer_begin(cudaStream_t s, int kind, double work) {
   KernelTimer* t = g_timer;
   if (!t || t->used + 2 > t->capacity || t->used / 2 >= 4096) return -1;
