@@ -84,11 +84,7 @@ void launch_z_3m(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   // 64x32 tiles, 4 warps of 32x16, 3 CTAs per SM (measured 40-41 TFLOP/s complex-equivalent
   // on 4096^3 against 33-35 for the four-multiplication 64x64 kernel)
   const dim3 g2(grid.x, unsigned(ceil_div(p.n, 32)), grid.z);
-  static const int st = getenv("BSE_GEMM_3M_ST") ? atoi(getenv("BSE_GEMM_3M_ST")) : 4;
-  if (st == 3) launch_z_3m_cfg<32, 8, 3, 3, CA, CB>(s, p, g2);
-  else if (st == 6) launch_z_3m_cfg<32, 8, 6, 3, CA, CB>(s, p, g2);
-  else if (st == 8) launch_z_3m_cfg<32, 8, 8, 3, CA, CB>(s, p, g2);
-  else launch_z_3m_cfg<32, 8, 4, 3, CA, CB>(s, p, g2);
+  launch_z_3m_cfg<32, 8, 4, 3, CA, CB>(s, p, g2);  // 3 or 4 stages measure alike; 6+ lose
 }
 
 void launch_z_any(cudaStream_t s, int opa, int opb, const ZGemmParams& p, dim3 grid) {

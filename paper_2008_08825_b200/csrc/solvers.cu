@@ -39,12 +39,9 @@ struct PhaseClock {
 }  // namespace
 
 int64_t recover_chunk_cols(const bse_ctx* c, int64_t n, int64_t min_cols, int parts) {
-  static const char* force = std::getenv("BSE_FORCE_CHUNKS");  // experiments: chunk w/o sink
-  static const char* ep = std::getenv("BSE_CHUNK_PARTS");
-  static const char* em = std::getenv("BSE_CHUNK_MIN");
-  if (ep) parts = std::atoi(ep);
-  if (em) min_cols = std::atoi(em);
-  if (!c->sink_v && !force) return n;
+  // two chunks: the first chunk's copy hides behind the second's compute; more chunks cost
+  // more in narrower GEMMs / TRSM launch chains than they hide (measured 2/4/8)
+  if (!c->sink_v) return n;
   const int64_t w = std::max<int64_t>(min_cols, ceil_div(ceil_div(n, parts), 64) * 64);
   return std::min<int64_t>(n, w);
 }
