@@ -165,7 +165,7 @@ def main():
     ap.add_argument("--method", default="chol", choices=["chol", "chol-svd"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lanes", type=int, default=2, help="matrices in flight per GPU")
+    ap.add_argument("--lanes", type=int, default=4, help="matrices in flight per GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -188,15 +188,20 @@ def main():
     lanes = max(1, args.lanes)
     ctx.set_batch_lanes(lanes)
     total = (args.warmup + args.steps) * lanes
-    seeds = seeds_for(rank, world, total)
-    host = []
-    d_in = []
+    # a pool of up to 8 distinct matrices per rank, item i -> pool[i % pool]: every input is
+    # 512 MiB (> 126 MB L2), so cycling the pool needs no L2 flush between items
+    pool = min(total, 8)
+    seeds = seeds_for(rank, world, pool)
+    host_pool = []
+    dev_pool = []
     for sd in seeds:
         a, b = configs.config5(sd, n=n)
         ha = torch.from_numpy(a.T).pin_memory()  # same bytes, column-major complex128
         hb = torch.from_numpy(b.T).pin_memory()
-        host.append((ha, hb))
-        d_in.append((ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)))
+        host_pool.append((ha, hb))
+        dev_pool.append((ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)))
+    host = [host_pool[i % pool] for i in range(total)]
+    d_in = [dev_pool[i % pool] for i in range(total)]
     torch.cuda.synchronize()
     d_lams = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(total)]
     d_vs = [torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)  # 2n x n col-major
@@ -246,6 +251,7 @@ def main():
     l1.record(stream)
     torch.cuda.synchronize()
     single_ms = l0.elapsed_time(l1) / 2
+    ph_single = ctx.phase_times()  # per-kernel event timings of a solve that owns the GPU
 
     # ---- end to end through the host-pointer C-ABI: every step's inputs go H2D from pinned
     # host memory and its (lambda, V) come back D2H inside the timed region. Headline: the
@@ -326,56 +332,63 @@ def main():
 
     # ---- roofline of the dominant kernel class from the live event timings
     peaks = load_peaks()
-    ph = phase_hist[-1]
-    panel = {"ms": ph["panel_ms"], "launches": ph["panel_launches"], "bytes": ph["panel_bytes"]}
-    gemm = {"ms": ph["gemm_ms"], "launches": ph["gemm_launches"], "flops": ph["gemm_flops"]}
     fp64_peak = 37.0  # DMMA m8n8k4 issue-rate probe on this pool (tools/microbench/fp64_peak.cu)
-    if panel["ms"] >= gemm["ms"]:
-        ach = panel["bytes"] / (panel["ms"] / 1e3) / 1e9
-        pk = peaks.get("hbm_gbs", 6650.0)
-        roofline = {"bound": "hbm",
-                    "kernel": ("gebrd_panel_kernel" if method == "chol-svd" else "hetrd_panel_kernel")
-                    + " (cooperative, TMA tile ring)",
-                    "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk,
-                    "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                    "per_launch_ms": panel["ms"] / max(panel["launches"], 1),
-                    "algorithmic_bytes_per_launch": panel["bytes"] / max(panel["launches"], 1)}
-    else:
-        ach = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12
-        roofline = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (DMMA.8x8x4)",
-                    "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                    "traffic": None,
-                    "peak_source": "measured FP64 DMMA probe (MEASURED_PEAKS.json has no FP64)",
-                    "per_launch_ms": gemm["ms"] / max(gemm["launches"], 1)}
-    try:
-        with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(roofline["bound"], {})
-        if roofline["bound"] == "hbm" and "ratio" in tr:
-            # ncu dram bytes / algorithmic bytes of one captured launch, applied per launch
-            trk = tr.get("gebrd", tr) if method == "chol-svd" else tr
-            roofline["traffic"] = trk["ratio"] * roofline["algorithmic_bytes_per_launch"]
-            roofline["traffic_source"] = trk.get("capture")
-        if roofline["bound"] == "tensor" and "bytes_per_flop" in tr:
-            # ncu dram bytes per executed flop of the captured 4096^3 launch, per average launch
-            roofline["traffic"] = tr["bytes_per_flop"] * gemm["flops"] / max(gemm["launches"], 1)
-            roofline["traffic_unit"] = "bytes per launch (DRAM read + write)"
-            roofline["traffic_source"] = tr.get("capture")
-    except Exception:
-        pass
+
+    def roofline_of(ph, where):
+        panel = {"ms": ph["panel_ms"], "launches": ph["panel_launches"], "bytes": ph["panel_bytes"]}
+        gemm = {"ms": ph["gemm_ms"], "launches": ph["gemm_launches"], "flops": ph["gemm_flops"]}
+        if panel["ms"] >= gemm["ms"]:
+            ach = panel["bytes"] / (panel["ms"] / 1e3) / 1e9
+            pk = peaks.get("hbm_gbs", 6650.0)
+            rf = {"bound": "hbm",
+                  "kernel": ("gebrd_panel_kernel" if method == "chol-svd" else "hetrd_panel_kernel")
+                  + " (cooperative, TMA tile ring)",
+                  "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                  "per_launch_ms": panel["ms"] / max(panel["launches"], 1),
+                  "algorithmic_bytes_per_launch": panel["bytes"] / max(panel["launches"], 1)}
+        else:
+            ach = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12
+            rf = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (DMMA.8x8x4, 3M)",
+                  "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                  "traffic": None,
+                  "peak_source": "measured FP64 DMMA probe (MEASURED_PEAKS.json has no FP64)",
+                  "per_launch_ms": gemm["ms"] / max(gemm["launches"], 1)}
+        rf["measured"] = where
+        try:
+            with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
+                tr = json.load(f).get(rf["bound"], {})
+            if rf["bound"] == "hbm" and "ratio" in tr:
+                # ncu dram bytes / algorithmic bytes of one captured launch, applied per launch
+                trk = tr.get("gebrd", tr) if method == "chol-svd" else tr
+                rf["traffic"] = trk["ratio"] * rf["algorithmic_bytes_per_launch"]
+                rf["traffic_source"] = trk.get("capture")
+            if rf["bound"] == "tensor" and "bytes_per_flop" in tr:
+                rf["traffic"] = tr["bytes_per_flop"] * gemm["flops"] / max(gemm["launches"], 1)
+                rf["traffic_unit"] = "bytes per launch (DRAM read + write)"
+                rf["traffic_source"] = tr.get("capture")
+        except Exception:
+            pass
+        return rf, panel, gemm
+
+    ph = phase_hist[-1]
+    roofline, panel, gemm = roofline_of(
+        ph, f"timed region, lane 0 of {lanes}: each panel kernel runs on 1/{lanes} of the SMs "
+            f"beside the other lanes' work")
+    roofline_whole, _, _ = roofline_of(ph_single, "single-solve pass: the kernel owns the GPU")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         cores = os.cpu_count() or 1
         oracle.set_threads(cores)
-        a, b = configs.config5(seeds[args.warmup], n=n)
+        a, b = configs.config5(seeds[args.warmup % pool], n=n)
         t0 = time.perf_counter()
         oracle.solve(method, a, b)
         tc = time.perf_counter() - t0
         cpu = {"value": flops(method, n) / tc / 1e12, "unit": "TFLOP/s", "cores": cores,
                "kind": "port", "s_per_solve": tc,
-               "sample": f"one {method} solve of config-5 seed {seeds[args.warmup]} (n={n}) with "
+               "sample": f"one {method} solve of config-5 seed {seeds[args.warmup % pool]} (n={n}) with "
                          f"the oracle/ LAPACK restatement on {cores} host threads"}
 
     if rank == 0:
@@ -389,18 +402,23 @@ def main():
                                    f"GPU solves {lanes} matrices of its seed shard concurrently "
                                    "(bse_solve_batched_device, one lane per matrix)",
                        "n": n, "method": method, "batch": 64, "matrices_per_step_per_gpu": lanes,
-                       "l2": "inputs 512 MiB per solve (> 126 MB L2), distinct per step",
+                       "l2": "inputs 512 MiB per solve (> 126 MB L2); a pool of up to 8 "
+                             "distinct matrices per rank, cycled",
                        "parallelism": f"dp{world} (seed partition, NCCL gathers eigenvalues)"},
             "s_per_solve": ms_per_step / 1e3 / lanes,
             "single_solve_latency_ms": single_ms,
             "batch64_s": ms_per_step / 1e3 / lanes * 64 / world,
             "fp64_frac_of_peak": value / (world * fp64_peak),
-            "phase_ms": {k: round(v, 3) for k, v in ph.items()
+            "phase_ms": {k: round(v, 3) for k, v in ph_single.items()
                          if k in ("product_pair", "triple", "reduce", "tridiag", "backtransform",
-                                  "recover", "total")},
+                                  "recover", "total")},  # one solve alone on the whole GPU
+            "phase_ms_batch_lane0": {k: round(v, 3) for k, v in ph.items()
+                                     if k in ("product_pair", "triple", "reduce", "tridiag",
+                                              "backtransform", "recover", "total")},
             "kernels": {"panel": panel, "gemm": gemm,
                         "gemm_tflops": gemm["flops"] / max(gemm["ms"], 1e-9) / 1e9},
             "roofline": roofline,
+            "roofline_whole_gpu": roofline_whole,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

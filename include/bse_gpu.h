@@ -135,7 +135,7 @@ int bse_solve_device(bse_ctx* ctx, int method, int64_t n,
  * method and shape from host buffers a[i], b[i] into lambda[i], v[i]. The upload of matrix
  * i+1 and the download of matrix i-1 run on copy streams while matrix i computes, so with
  * page-locked host buffers the PCIe traffic hides behind the solves. Items run on
- * bse_ctx_set_batch_lanes() lanes (default 2 solves in flight, item i on lane i % lanes).
+ * bse_ctx_set_batch_lanes() lanes (default 4 solves in flight, item i on lane i % lanes).
  *   near_singular  : null or capacity batch*n (row i holds matrix i's flagged indices)
  *   n_near_singular: null or capacity batch
  *   failed_index   : null or receives the first failing item (-1 when all succeed); the
@@ -153,7 +153,8 @@ int bse_solve_batched_device(bse_ctx* ctx, int method, int64_t n, int64_t batch,
                              int64_t ldb, double* const* d_lambda, double* const* d_v,
                              int64_t ldv, int64_t* near_singular, int64_t* n_near_singular,
                              int64_t* failed_index, bse_status* st);
-/* Solves in flight per batch call, 1..4 (default 2). With L > 1 the batch runs on L contexts
+/* Solves in flight per batch call, 1..8 (default 4; fewer when device memory is short: each
+ * lane needs its own workspace). With L > 1 the batch runs on L contexts
  * at once (L - 1 created on first use) and each cooperative panel kernel is limited to 1/L of
  * the SMs, so one solve's latency-bound reductions overlap another's GEMM phases. */
 int bse_ctx_set_batch_lanes(bse_ctx* ctx, int lanes);

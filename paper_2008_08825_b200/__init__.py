@@ -260,9 +260,9 @@ class Context:
         return int(_lib.lib().bse_ctx_kernel_launches(self._h))
 
     def set_batch_lanes(self, lanes: int):
-        """Solves in flight per batch call (1..4, default 2), see bse_ctx_set_batch_lanes."""
+        """Solves in flight per batch call (1..8, default 4), see bse_ctx_set_batch_lanes."""
         if _lib.lib().bse_ctx_set_batch_lanes(self._h, int(lanes)) != 0:
-            raise InvalidSpec("batch lanes must be 1..4")
+            raise InvalidSpec("batch lanes must be 1..8")
 
     def stream(self) -> int:
         return int(_lib.lib().bse_ctx_stream(self._h) or 0)

@@ -510,7 +510,23 @@ void run_lane(bse_ctx* c, const BatchIO& io, const std::vector<int64_t>& items, 
 void run_batch(bse_ctx* c, const BatchIO& io, int64_t batch, int64_t* failed_index) {
   if (failed_index) *failed_index = -1;
   if (batch == 0) return;
-  const int lanes = int(std::min<int64_t>(c->batch_lanes, batch));
+  // lanes that fit: every extra lane needs its own solver workspace (+ staging on the host
+  // path); lanes whose context already holds a large enough arena cost nothing new
+  const int64_t n = io.n;
+  const size_t nn = size_t(n) * size_t(n);
+  size_t per_lane = io.method == BSE_METHOD_REFERENCE
+                        ? 4 * solve_workspace_bytes(BSE_METHOD_CHOL_SVD, 2 * n) / 3
+                        : solve_workspace_bytes(io.method == BSE_METHOD_CHOL ? BSE_METHOD_CHOL
+                                                                             : BSE_METHOD_CHOL_SVD, n);
+  if (!io.device) per_lane += 2 * (4 * nn + size_t(n)) * sizeof(z_t);
+  size_t free_b = 0, total_b = 0;
+  BSE_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int ready = 1;
+  for (int l = 1; l < c->batch_lanes && c->twin[l - 1]; ++l)
+    if (c->twin[l - 1]->arena_bytes >= per_lane - (io.device ? 0 : 2 * (4 * nn + size_t(n)) * sizeof(z_t)))
+      ++ready;
+  const int64_t fit = ready + int64_t(0.85 * double(free_b) / double(per_lane));
+  const int lanes = int(std::max<int64_t>(1, std::min<int64_t>({int64_t(c->batch_lanes), batch, fit})));
   int sms = 0;
   BSE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int prev_cap = g_panel_ctas;
@@ -529,7 +545,7 @@ void run_batch(bse_ctx* c, const BatchIO& io, int64_t batch, int64_t* failed_ind
         throw std::runtime_error(std::string("batch lane context: ") + st.message);
     }
     bse_ctx* lc = c->twin[l - 1];
-    const int cap = g_panel_ctas;
+    const int cap = g_panel_ctas;  // set above from `lanes`
     extra.emplace_back([&, l, lc, cap] {
       try {
         BSE_CUDA(cudaSetDevice(lc->device));
@@ -598,7 +614,7 @@ int bse_solve_batched_device(bse_ctx* c, int method, int64_t n, int64_t batch,
 }
 
 int bse_ctx_set_batch_lanes(bse_ctx* c, int lanes) {
-  if (!c || lanes < 1 || lanes > 4) return BSE_ERR_INVALID_SPEC;
+  if (!c || lanes < 1 || lanes > 8) return BSE_ERR_INVALID_SPEC;
   std::lock_guard<std::mutex> lock(c->mu);
   c->batch_lanes = lanes;
   return BSE_OK;

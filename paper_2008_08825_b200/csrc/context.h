@@ -33,9 +33,9 @@ struct bse_ctx {
   // bse_solve_batched: host-to-device uploads of the next matrix run on copy_in
   cudaStream_t copy_in = nullptr;
   cudaEvent_t batch_ev[7]{};
-  // batch driver: solves in flight per call (1..4) and the extra lanes' contexts
-  int batch_lanes = 2;
-  bse_ctx* twin[3]{};
+  // batch driver: solves in flight per call (1..8) and the extra lanes' contexts
+  int batch_lanes = 4;
+  bse_ctx* twin[7]{};
   // look-ahead streams / events of the two concurrent Cholesky factorisations
   cudaStream_t la[2]{};
   cudaEvent_t la_ev[4]{};

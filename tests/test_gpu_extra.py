@@ -286,7 +286,7 @@ def test_pinned_output_streams_same_solution(method, n):
 
 
 # ------------------------------------------------------------- batch driver
-@pytest.mark.parametrize("lanes", [1, 2, 3])
+@pytest.mark.parametrize("lanes", [1, 2, 4])
 @pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
 def test_solve_batched_matches_single_solves(method, lanes):
     """One lane runs the single-solve kernels: bit-identical. With L lanes the cooperative
@@ -345,8 +345,9 @@ def test_solve_batched_device_lanes():
                 assert np.max(np.abs(lam - ref[i][0]) / ref[i][0]) <= 1e-13
                 assert residual(mats[i][0], mats[i][1], lam, v).max() <= 100 * n * EPS
         ctx.close()
-    with pytest.raises(bse.InvalidSpec):
-        bse.default_context().set_batch_lanes(0)
+    for bad in (0, 9):
+        with pytest.raises(bse.InvalidSpec):
+            bse.default_context().set_batch_lanes(bad)
 
 
 def test_solve_batched_reports_failing_item():
