@@ -264,7 +264,7 @@ def main():
         import ctypes
         L = bse._lib.lib()
         st = bse.Status()
-        nv = min(args.steps * lanes, 8)  # distinct pinned outputs (reused cyclically beyond 8)
+        nv = lanes  # pinned outputs: item i -> i % lanes (items of one lane run in order)
         hv = [torch.empty((n, 2 * n), dtype=torch.complex128).pin_memory() for _ in range(nv)]
         hl = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(nv)]
         ns = np.zeros((total, n), dtype=np.int64)
