@@ -27,12 +27,12 @@ template <bool CA, bool CB>
 void launch_z(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   using T = ZGemmTile<kBM, kBN, kBK, kWM, kWN, kST, CA, CB>;
   auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWN, kST, CA, CB>;
-  static bool configured = false;  // per template instance
-  if (!configured) {
+  static const bool configured = [&] {  // one-time setup per template instance (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
-    configured = true;
-  }
+    return true;
+  }();
+  (void)configured;
   kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
   BSE_LAUNCH_CHECK();
 }
@@ -46,12 +46,12 @@ template <bool CA, bool CB>
 void launch_z_short(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   using T = ZGemmTile<kBM, kBN, kBK, kWM, kWNs, kSTs, CA, CB>;
   auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWNs, kSTs, CA, CB, kMinBs>;
-  static bool configured = false;
-  if (!configured) {
+  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
-    configured = true;
-  }
+    return true;
+  }();
+  (void)configured;
   kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
   BSE_LAUNCH_CHECK();
 }
@@ -62,12 +62,12 @@ template <int BN, int BK, int ST, int MINB, bool CA, bool CB>
 void launch_z_3m_cfg(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   using T = ZGemmTile<kBM, BN, BK, kWM, kWNs, ST, CA, CB>;
   auto kern = zgemm_dmma_kernel<kBM, BN, BK, kWM, kWNs, ST, CA, CB, MINB, true>;
-  static bool configured = false;
-  if (!configured) {
+  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
-    configured = true;
-  }
+    return true;
+  }();
+  (void)configured;
   kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
   BSE_LAUNCH_CHECK();
 }
@@ -226,12 +226,12 @@ void dgemm_nn(cudaStream_t s, int64_t m, int64_t n, int64_t k, double alpha, con
   constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, ST = 3;
   using T = DGemmTile<BM, BN, BK, WM, WN, ST>;
   auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, ST>;
-  static bool configured = false;
-  if (!configured) {
+  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
-    configured = true;
-  }
+    return true;
+  }();
+  (void)configured;
   DGemmParams p{};
   p.m = m; p.n = n; p.k = k;
   p.A = A; p.lda = lda; p.B = B; p.ldb = ldb; p.C = C; p.ldc = ldc;
@@ -293,12 +293,12 @@ __global__ void __launch_bounds__(256) ztrtri_diag_kernel(int64_t n, const z_t* 
 void ztrtri_diag_blocks(cudaStream_t s, int64_t n, const z_t* L, int64_t ldl, int nb, z_t* inv) {
   const int64_t nblk = ceil_div(n, nb);
   const size_t smem = size_t(2) * nb * (nb + 1) * sizeof(z_t);
-  static bool configured = false;
-  if (!configured) {
+  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(ztrtri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
-    configured = true;
-  }
+    return true;
+  }();
+  (void)configured;
   ztrtri_diag_kernel<<<unsigned(nblk), 256, smem, s>>>(n, L, ldl, nb, inv);
   BSE_LAUNCH_CHECK();
 }
@@ -408,14 +408,15 @@ void ztrsm_lower(cudaStream_t s, int side, int op, int64_t n, int64_t other, con
 }
 
 CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {  // thread-safe one-time lookup
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     cudaDriverEntryPointQueryResult q;
-    BSE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+    BSE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&f),
                                      cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !encode)
+    if (q != cudaDriverEntryPointSuccess || !f)
       throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
-  }
+    return f;
+  }();
   CUtensorMap map;
   const cuuint64_t dims[2] = {cuuint64_t(2 * n), cuuint64_t(n)};
   const cuuint64_t strides[1] = {cuuint64_t(lda) * sizeof(z_t)};

@@ -601,17 +601,22 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   a.nch = nch;
   const size_t smem = (size_t(kRing) * kTile + kRing + 2 * kT + 2 * 8 * kT + 4 * (kNB + 1) + 2 * kT) *
                           sizeof(z_t) + kTabMax * sizeof(int) + 8 * sizeof(double) + 128;
-  static int blocks_per_sm = -1, num_sms = 0;
-  if (blocks_per_sm < 0) {
+  struct Occ {
+    int blocks_per_sm, num_sms;
+  };
+  static const Occ occ = [&] {  // one-time setup (thread-safe: batch lanes)
+    Occ o{0, 0};
     BSE_CUDA(cudaFuncSetAttribute(gebrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
     int dev;
     BSE_CUDA(cudaGetDevice(&dev));
-    BSE_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-    BSE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, gebrd_panel_kernel,
+    BSE_CUDA(cudaDeviceGetAttribute(&o.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    BSE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks_per_sm, gebrd_panel_kernel,
                                                            kThreads, smem));
-    if (blocks_per_sm < 1) throw std::runtime_error("gebrd: kernel cannot be resident");
-  }
+    return o;
+  }();
+  const int blocks_per_sm = occ.blocks_per_sm, num_sms = occ.num_sms;
+  if (blocks_per_sm < 1) throw std::runtime_error("gebrd: kernel cannot be resident");
   const z_t mone = {-1.0, 0.0}, one = {1.0, 0.0};
   const char* trace_path = getenv("BSE_GEBRD_TRACE");
   const size_t trace_n = size_t(ceil_div(n, kNB)) * kNB * 2 * 8;

@@ -563,18 +563,22 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   const size_t smem = (size_t(kRing) * kRingT * kRingT + kRing + 4 * kT + 2 * (8 * kT + kT) + 2 * NB +
                        2 * kT + 2 * NB + 8) * sizeof(z_t) + kTabMax * sizeof(int) + 8 * sizeof(double) +
                       128;
-  static int blocks_per_sm = -1;
-  static int num_sms = 0;
-  if (blocks_per_sm < 0) {
+  struct Occ {
+    int blocks_per_sm, num_sms;
+  };
+  static const Occ occ = [&] {  // one-time setup (thread-safe: batch lanes)
+    Occ o{0, 0};
     BSE_CUDA(cudaFuncSetAttribute(hetrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
     int dev;
     BSE_CUDA(cudaGetDevice(&dev));
-    BSE_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-    BSE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hetrd_panel_kernel,
+    BSE_CUDA(cudaDeviceGetAttribute(&o.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    BSE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks_per_sm, hetrd_panel_kernel,
                                                            kThreads, smem));
-    if (blocks_per_sm < 1) throw std::runtime_error("hetrd: kernel cannot be resident");
-  }
+    return o;
+  }();
+  const int blocks_per_sm = occ.blocks_per_sm, num_sms = occ.num_sms;
+  if (blocks_per_sm < 1) throw std::runtime_error("hetrd: kernel cannot be resident");
   if (n == 1) {
     set_last_diag_kernel<<<1, 32, 0, s>>>(A, lda, n, d);
     BSE_LAUNCH_CHECK();

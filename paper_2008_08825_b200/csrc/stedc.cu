@@ -907,12 +907,12 @@ void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, vo
 
   std::vector<MergeDesc> hmd;
   std::vector<int> htile;
-  static bool configured = false;
-  if (!configured) {
+  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(stedc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(GT::SMEM)));
-    configured = true;
-  }
+    return true;
+  }();
+  (void)configured;
   for (int lvl = L - 1; lvl >= 0; --lvl) {
     const int nm = 1 << lvl;
     hmd.resize(nm);
