@@ -440,3 +440,23 @@ def test_large_solve_device_residual(method):
         if ref is None:
             ref = got
         assert np.array_equal(got, ref)  # bit-deterministic run to run
+
+
+def test_solve_batched_edge_cases():
+    """Batch driver corner cases: one item on a multi-lane context, tiny sizes, several
+    failing items in different lanes (the first one is reported), lanes > items."""
+    ctx = bse.Context(0)
+    ctx.set_batch_lanes(4)
+    one = bse.from_blocks(np.array([[2.0]]), np.array([[1.0]]))
+    r = bse.solve_batched(bse.Method.CholSvd, [one], ctx=ctx)
+    assert len(r) == 1 and abs(r[0].lambda_[0] - np.sqrt(3.0)) < 1e-13
+    hs = [bse.from_blocks(*configs.config2(s, n=65)) for s in range(6)]
+    out = bse.solve_batched(bse.Method.Chol, hs, ctx=ctx)
+    for h, x in zip(hs, out):
+        assert residual(h.a, h.b, x.lambda_, x.v).max() <= 100 * 65 * EPS
+    good = hs[0]
+    bad = bse.from_blocks(np.eye(65, dtype=complex), 2 * np.eye(65, dtype=complex))
+    with pytest.raises(bse.BatchError) as ei:
+        bse.solve_batched(bse.Method.Chol, [good, good, bad, bad, good], ctx=ctx)
+    assert ei.value.index == 2 and len(ei.value.results) == 2
+    ctx.close()
