@@ -790,24 +790,24 @@ int bse_hermitian_eig(bse_ctx* c, int64_t n, const double* m, int64_t ldm, doubl
       throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "hermitian_eig: bad dimensions"};
     const size_t nn = size_t(n) * size_t(n);
     const size_t bytes = nn * 2 * sizeof(z_t) + nn * sizeof(double) + stedc_workspace_bytes(n) +
-                         hetrd_workspace_bytes(n) + unmtr_workspace_bytes(n, n) +
+                         tridiag_workspace_bytes(n) + unmtr_workspace_bytes(n, n) +
                          size_t(n) * 48 + 4096;
     Bump w = arena(c, bytes);
     z_t* dM = w.take<z_t>(nn);
     z_t* dZ = w.take<z_t>(nn);
     double* Z = w.take<double>(nn);
     void* ws_st = w.take<char>(stedc_workspace_bytes(n));
-    void* ws_ht = w.take<char>(hetrd_workspace_bytes(n));
+    void* ws_ht = w.take<char>(tridiag_workspace_bytes(n));
     void* ws_um = w.take<char>(unmtr_workspace_bytes(n, n));
     double* d = w.take<double>(n);
     double* e = w.take<double>(n);
     z_t* tau = w.take<z_t>(n);
     int* info = w.take<int>(2);
     h2d(c, dM, n, m, ldm, n, n);
-    zhetrd_lower(c->stream, n, dM, n, d, e, tau, ws_ht);
+    tridiag_reduce(c->stream, n, dM, n, d, e, tau, ws_ht);
     dstedc(c->stream, n, d, e, Z, ws_st, info);
     real_to_complex(c->stream, n, n, Z, n, dZ, n);
-    zunmtr_lower(c->stream, n, dM, n, tau, dZ, n, n, ws_um);
+    tridiag_back(c->stream, n, dM, n, tau, ws_ht, dZ, n, n, ws_um);
     int h = 0;
     BSE_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     BSE_CUDA(cudaMemcpyAsync(values, d, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, c->stream));

@@ -140,7 +140,7 @@ void product_pair_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_
 
 size_t heevd_workspace_bytes(int64_t n) {
   const size_t nn = size_t(n) * size_t(n);
-  return nn * sizeof(double) + stedc_workspace_bytes(n) + hetrd_workspace_bytes(n) +
+  return nn * sizeof(double) + stedc_workspace_bytes(n) + tridiag_workspace_bytes(n) +
          unmtr_workspace_bytes(n, n) + size_t(n) * 48 + 8 * 256;
 }
 
@@ -150,15 +150,15 @@ void heevd_dev(cudaStream_t s, int64_t n, z_t* M, int64_t ldm, double* w, z_t* Z
                Bump& b) {
   double* Zr = b.take<double>(size_t(n) * size_t(n));
   void* ws_st = b.take<char>(stedc_workspace_bytes(n));
-  void* ws_ht = b.take<char>(hetrd_workspace_bytes(n));
+  void* ws_ht = b.take<char>(tridiag_workspace_bytes(n));
   void* ws_um = b.take<char>(unmtr_workspace_bytes(n, n));
   double* e = b.take<double>(n);
   z_t* tau = b.take<z_t>(n);
   int* info = b.take<int>(1);
-  zhetrd_lower(s, n, M, ldm, w, e, tau, ws_ht);
+  tridiag_reduce(s, n, M, ldm, w, e, tau, ws_ht);
   dstedc(s, n, w, e, Zr, ws_st, info);
   real_to_complex(s, n, n, Zr, n, Z, ldz);
-  zunmtr_lower(s, n, M, ldm, tau, Z, ldz, n, ws_um);
+  tridiag_back(s, n, M, ldm, tau, ws_ht, Z, ldz, n, ws_um);
   check_info(s, info, BSE_ERR_CONVERGENCE_FAILURE, 0, "zheevd failed to converge (info=", false);
 }
 

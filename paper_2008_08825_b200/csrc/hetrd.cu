@@ -653,9 +653,13 @@ constexpr int kBT = 128;  // reflectors per applied block (the K of the update G
 //   mode 0 (zhetrd 'L'): v_j(j+1) = 1, v_j(r) = A(r, j)  for r > j+1
 //   mode 1 (zgebrd Q)  : v_j(j)   = 1, v_j(r) = A(r, j)  for r > j
 //   mode 2 (zgebrd P)  : u_j(j+1) = 1, u_j(c) = A(j, c)  for c > j+1 (row storage)
+//   mode 3 (he2hb 'L') : v_j(j+kBand2) = 1, v_j(r) = A(r, j)  for r > j+kBand2 (hetrd2.cu)
+__device__ __host__ __forceinline__ int reflector_offset(int mode) {
+  return mode == 1 ? 0 : (mode == 3 ? kBand2 : 1);
+}
 __global__ void build_vall_kernel(const z_t* __restrict__ A, int64_t lda, int64_t n,
                                   int64_t nref, int64_t ncol, int mode, z_t* __restrict__ Vall) {
-  const int off = mode == 1 ? 0 : 1;
+  const int off = reflector_offset(mode);
   const int64_t total = n * ncol;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -712,7 +716,7 @@ size_t unmtr_workspace_bytes(int64_t n, int64_t ncols) {
 void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z_t* A,
                       int64_t lda, const z_t* tau, z_t* Z, int64_t ldz, int64_t ncols, void* ws) {
   if (nref <= 0 || ncols <= 0) return;
-  const int off = mode == 1 ? 0 : 1;
+  const int off = reflector_offset(mode);
   const int64_t nblk = ceil_div(nref, kBT);
   const int64_t ncol = nblk * kBT;
   z_t* Vall = reinterpret_cast<z_t*>(ws);

@@ -1,0 +1,695 @@
+// hetrd2.cu — two-stage Householder tridiagonalisation of a Hermitian matrix (lower storage)
+// and its back-transformation, an alternative to hetrd.cu's one-stage reduction for the
+// zheevd('V','L') replacement (proj/src/backend.cpp:34).
+//
+// The one-stage panels are latency-bound (two grid barriers per column). The two-stage form
+// moves the O(n^3) work to DMMA GEMMs and leaves an O(n^2 b) bulge chase:
+//
+//  stage 1  he2hb  (LAPACK zhetrd_he2hb structure): per panel of b = kBand2 columns, the
+//           panel below the band is QR-factored by one cooperative kernel (rows in registers,
+//           two grid barriers per column over <= n/256 CTAs) that also forms T and V T; then
+//           X = A22 (V T) as two triangular DMMA GEMMs over the lower triangle,
+//           W = X - 1/2 V (T^H V^H X), and the her2k A22 -= V W^H + W V^H (lower tiles only).
+//  stage 2  hb2st  bulge chasing on a packed band (2b rows per column, L2-resident). Task
+//           (s, j) of sweep s: right-apply the previous reflector to the bulge block Bk_j,
+//           annihilate its first column, left-apply to the rest of Bk_j, two-sided update of
+//           the diagonal block D_j. One warp per sweep, smem-staged 32x32 blocks; sweep s runs
+//           task j once sweep s-1 has finished task j+1 (progress counters, acquire/release).
+//  back     Z <- Q1 Q2 Z. Q2: the chase reflectors in groups of 32 sweeps x one task index,
+//           groups ordered (sweep block descending, task ascending), each thread keeping a
+//           64-row window of one column in registers and streaming down the column; Q1: the
+//           stage-1 reflectors through apply_reflectors (mode 3, compact WY on DMMA).
+//
+// The bookkeeping (task extents, schedule rule, group order) is modelled in numpy by
+// tools/two_stage_model.py. Every sum has a fixed order: results are bit-deterministic.
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "blas.h"
+#include "gemm.cuh"
+#include "hetrd.h"
+#include "ops.h"
+
+namespace bseg {
+
+namespace {
+constexpr int kB = kBand2;       // band width
+constexpr int kQrT = 256;        // panel rows per QR CTA (one row per thread)
+constexpr int kLdab = 2 * kB;    // packed band: offsets 0 .. 2b-1 below the diagonal
+constexpr int kChW = 4;          // chase warps per CTA
+constexpr int kBp = kB + 1;      // padded smem block stride
+constexpr int kQ2Rows = 64;      // back-transform window rows (b + 32 - 1, padded)
+constexpr int kQ2Res = 4;        // row residues per column (lanes per column)
+constexpr int kQ2Reg = kQ2Rows / kQ2Res;  // window rows per thread
+constexpr int kQ2Warps = 4;      // warps per back-transform CTA (8 columns each)
+
+__device__ __forceinline__ z_t zdiv1(z_t a) {
+  const double den = a.x * a.x + a.y * a.y;
+  return make_double2(a.x / den, -a.y / den);
+}
+
+// zlarfg on (alpha, ||x||^2): beta (real), tau, scale = 1 / (alpha - beta) (1 if tau == 0).
+__device__ __forceinline__ void larfg2(z_t alpha, double xnorm2, double& beta, z_t& tau,
+                                       z_t& scale) {
+  if (xnorm2 == 0.0 && alpha.y == 0.0) {
+    beta = alpha.x;
+    tau = make_double2(0.0, 0.0);
+    scale = make_double2(1.0, 0.0);
+    return;
+  }
+  const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2);
+  beta = alpha.x >= 0.0 ? -nrm : nrm;
+  tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+  scale = zdiv1(make_double2(alpha.x - beta, alpha.y));
+}
+
+__device__ __forceinline__ z_t shfl_z(z_t v, int o) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, o);
+  v.y = __shfl_xor_sync(0xffffffffu, v.y, o);
+  return v;
+}
+}  // namespace
+
+// ------------------------------------------------------------------------ stage 1: he2hb
+struct QrArgs {
+  z_t* P;          // panel (m x kB) inside A
+  int64_t ldp, m;
+  int k;           // reflectors: min(m, kB)
+  z_t* VW;         // V -> VW[:, 0:kB]
+  z_t* WV;         //   and WV[:, kB:2kB]
+  z_t* VT;         // V T (m x kB)
+  int64_t ldw;
+  z_t* T;          // kB x kB upper (ld kB)
+  z_t* tau;        // kB
+  double* normp;   // gridDim.x partial norms
+  z_t* alphab;     // alpha of the current column
+  z_t* part;       // gridDim.x x kB partial sums
+  unsigned* bar;   // grid barrier counter (zeroed)
+};
+
+// Householder QR of the m x kB panel (zgeqr2 column order, zlarfg reflectors), V and T
+// (zlarft forward/columnwise) and V T. Thread = panel row, its kB entries in registers.
+// Per column: (1) partial norms + alpha -> grid barrier -> (2) reflector (redundantly per
+// CTA), v, partial w = v^H P(:, c>j) and g = V(:, i<j)^H v in one kB-slot vector ->
+// grid barrier -> (3) totals (fixed order), rank-1 update, T column.
+__global__ void __launch_bounds__(kQrT, 1) he2hb_qr_kernel(const __grid_constant__ QrArgs a) {
+  GridBarrier grid(a.bar);
+  __shared__ z_t Ts[kB * kB];
+  __shared__ z_t wred[kQrT / 32][kB];
+  __shared__ z_t wsum[kB];
+  __shared__ z_t taus[kB];
+  __shared__ double dred[kQrT / 32 + 2];
+  __shared__ z_t alpha_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int64_t r = int64_t(blockIdx.x) * kQrT + tid;
+  const bool valid = r < a.m;
+  const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
+  z_t p[kB];
+#pragma unroll
+  for (int c = 0; c < kB; ++c) p[c] = valid ? a.P[r + c * a.ldp] : zero;
+  for (int e = tid; e < kB * kB; e += kQrT) Ts[e] = zero;
+  if (tid < kB) taus[tid] = zero;
+
+#pragma unroll
+  for (int j = 0; j < kB; ++j) {
+    if (j >= a.k) break;
+    // (1) partial ||P(j+1:, j)||^2 and alpha = P(j, j)
+    const double bs = block_sum((valid && r > j) ? zabs2(p[j]) : 0.0, dred);
+    if (tid == 0) a.normp[blockIdx.x] = bs;
+    if (r == j) *a.alphab = p[j];
+    grid.sync();
+    // (2) reflector
+    if (warp == 0) {
+      double x = 0.0;
+      for (int g = lane; g < G; g += 32) x += a.normp[g];
+      x = warp_sum(x);
+      if (lane == 0) {
+        dred[kQrT / 32] = x;
+        alpha_s = *a.alphab;
+      }
+    }
+    __syncthreads();
+    double beta;
+    z_t tau, scale;
+    larfg2(alpha_s, dred[kQrT / 32], beta, tau, scale);
+    z_t v = zero;
+    if (valid) v = (r == j) ? one : (r > j ? zmul(scale, p[j]) : zero);
+    if (valid && r > j) p[j] = v;
+    if (r == j) p[j] = make_double2(beta, 0.0);
+    // slot c > j: conj(v) P(r, c); slot i < j: conj(V(r, i)) v ; slot j: 0
+    z_t sl[16], sh[16];
+#pragma unroll
+    for (int c = 0; c < kB; ++c) {
+      z_t t = zero;
+      if (c > j) {
+        t = zcmul(v, p[c]);
+      } else if (c < j) {
+        const z_t vi = r > c ? p[c] : (r == c ? one : zero);
+        t = zcmul(vi, v);
+      }
+      if (c < 16) sl[c] = t; else sh[c - 16] = t;
+    }
+    __syncthreads();  // re-converge before the butterflies
+    const z_t tl = warp_transpose_zsum16(sl);  // lane l: slot l >> 1
+    const z_t th = warp_transpose_zsum16(sh);  // lane l: slot 16 + (l >> 1)
+    if ((lane & 1) == 0) {
+      wred[warp][lane >> 1] = tl;
+      wred[warp][16 + (lane >> 1)] = th;
+    }
+    __syncthreads();
+    if (tid < kB) {
+      z_t t = wred[0][tid];
+#pragma unroll
+      for (int w = 1; w < kQrT / 32; ++w) t = zadd(t, wred[w][tid]);
+      a.part[int64_t(blockIdx.x) * kB + tid] = t;
+    }
+    grid.sync();
+    // (3) totals, update, T(:, j)
+    if (tid < kB) {
+      z_t t = zero;
+      for (int g = 0; g < G; ++g) t = zadd(t, a.part[int64_t(g) * kB + tid]);
+      wsum[tid] = t;
+    }
+    __syncthreads();
+    const z_t ct = zconj(tau);
+#pragma unroll
+    for (int c = j + 1; c < kB; ++c) p[c] = zsub(p[c], zmul(zmul(ct, v), wsum[c]));
+    if (tid < kB) {
+      z_t t = zero;
+      if (tid < j) {  // T(i, j) = -tau sum_{i' = i}^{j-1} T(i, i') g(i')
+        for (int i2 = tid; i2 < j; ++i2) zfma(t, Ts[tid + i2 * kB], wsum[i2]);
+        t = zscale(zmul(tau, t), -1.0);
+      } else if (tid == j) {
+        t = tau;
+        taus[j] = tau;
+      }
+      if (tid <= j) Ts[tid + j * kB] = t;
+    }
+  }
+  __syncthreads();
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < kB; ++c) a.P[r + c * a.ldp] = p[c];
+    z_t vx[kB];
+#pragma unroll
+    for (int c = 0; c < kB; ++c) {
+      vx[c] = c < a.k ? (r > c ? p[c] : (r == c ? one : zero)) : zero;
+      a.VW[r + c * a.ldw] = vx[c];
+      a.WV[r + (kB + c) * a.ldw] = vx[c];
+    }
+#pragma unroll
+    for (int c = 0; c < kB; ++c) {
+      z_t t = zero;
+#pragma unroll
+      for (int i = 0; i <= c; ++i) zfma(t, vx[i], Ts[i + c * kB]);
+      a.VT[r + c * a.ldw] = t;
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int e = tid; e < kB * kB; e += kQrT) a.T[e] = Ts[e];
+    if (tid < kB) a.tau[tid] = taus[tid];
+  }
+}
+
+// W = X - 1/2 V (T^H Y), Y = V^H X (kB x kB). Writes W to VW[:, kB:2kB] and WV[:, 0:kB].
+// Thread = (row, column); every CTA forms M = T^H Y in shared memory.
+__global__ void __launch_bounds__(256) he2hb_w_kernel(int64_t m, const z_t* __restrict__ X,
+                                                      const z_t* __restrict__ Y,
+                                                      const z_t* __restrict__ T, z_t* VW,
+                                                      z_t* WV, int64_t ldw) {
+  __shared__ z_t Ms[kB * kBp];
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
+    const int i = e % kB, c = e / kB;
+    z_t t = make_double2(0.0, 0.0);
+    for (int q = 0; q <= i; ++q) zcfma(t, T[q + i * kB], Y[q + c * kB]);  // T upper
+    Ms[i + c * kBp] = t;
+  }
+  __syncthreads();
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m * kB) return;
+  const int64_t r = e % m;
+  const int c = int(e / m);
+  z_t acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+  for (int i = 0; i < kB; ++i) zfma(acc, VW[r + i * ldw], Ms[i + c * kBp]);
+  const z_t x = X[r + c * ldw];
+  const z_t w = make_double2(x.x - 0.5 * acc.x, x.y - 0.5 * acc.y);
+  VW[r + (kB + c) * ldw] = w;
+  WV[r + c * ldw] = w;
+}
+
+// Packs the lower band (offsets 0..kB) of A into AB (kLdab per column; offsets > kB zero),
+// diagonal real.
+__global__ void band_pack_kernel(int64_t n, const z_t* __restrict__ A, int64_t lda,
+                                 z_t* __restrict__ AB) {
+  const int64_t total = n * kLdab;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int o = int(e % kLdab);
+    const int64_t c = e / kLdab;
+    z_t v = make_double2(0.0, 0.0);
+    if (o <= kB && c + o < n) {
+      v = A[(c + o) + c * lda];
+      if (o == 0) v.y = 0.0;
+    }
+    AB[e] = v;
+  }
+}
+
+// ------------------------------------------------------------------------ stage 2: hb2st
+struct ChaseArgs {
+  z_t* AB;        // packed band, kLdab per column
+  int64_t n;
+  double* e;      // e[s] = beta of task (s, 0)
+  z_t* V2;        // [j][s][kB] reflectors (v[0] = 1), zero padded
+  z_t* tau2;      // [j][s]
+  int* prog;      // tasks finished per sweep (zeroed)
+  int nwarps;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Bulge chasing, one warp per sweep (sweeps round-robin over the warps of a cooperative grid,
+// so every sweep a warp waits on is owned by a resident warp). Lane r owns row r of the
+// 32x32 blocks for row-wise products and column r for column-wise ones; sB / sD are the bulge
+// block Bk_j and the (Hermitian-expanded) diagonal block D_j.
+__global__ void __launch_bounds__(32 * kChW, 1) hb2st_kernel(const __grid_constant__ ChaseArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  z_t* sB = reinterpret_cast<z_t*>(smraw) + warp * (2 * kB * kBp + 3 * kB);
+  z_t* sD = sB + kB * kBp;
+  z_t* sv = sD + kB * kBp;  // current reflector
+  z_t* sw = sv + kB;        // two-sided w
+  z_t* svp = sw + kB;       // previous reflector of the sweep
+  const int64_t n = a.n;
+  const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
+  const int gw = blockIdx.x * kChW + warp;
+  for (int64_t s = gw; s < n - 1; s += a.nwarps) {
+    const int nt = int(ceil_div(n - 1 - s, kB));
+    const int ntp = s > 0 ? int(ceil_div(n - s, kB)) : 0;  // tasks of sweep s-1
+    z_t taup = zero;
+    for (int j = 0; j < nt; ++j) {
+      if (s > 0) {
+        const int need = min(j + 2, ntp);
+        while (ld_acquire(a.prog + s - 1) < need) {
+        }
+      }
+      __syncwarp();
+      const int64_t lo = s + 1 + int64_t(j) * kB;
+      const int L = int(min64(kB, n - lo));
+      const int r = lane;
+      // D_j (Hermitian expanded, zero outside L x L)
+      for (int c = 0; c < kB; ++c) {
+        z_t x = zero;
+        if (c < L && r >= c && r < L) x = a.AB[(r - c) + (lo + c) * kLdab];
+        if (r == c) x.y = 0.0;
+        if (r >= c) sD[c * kBp + r] = x;  // each element written once (lower by its row's
+        if (r > c) sD[r * kBp + c] = zconj(x);  // lane, the mirror by the column's lane)
+      }
+      z_t xr;  // column to annihilate (row r)
+      const int64_t plo = lo - kB;
+      if (j > 0) {
+        for (int c = 0; c < kB; ++c)
+          sB[c * kBp + r] = r < L ? a.AB[(kB + r - c) + (plo + c) * kLdab] : zero;
+        __syncwarp();
+        // right-apply the previous reflector: Bk -= taup (Bk vp) vp^H (row-wise, lane = row)
+        z_t u = zero;
+        for (int c = 0; c < kB; ++c) zfma(u, sB[c * kBp + r], svp[c]);
+        const z_t tu = zmul(taup, u);
+        for (int c = 0; c < kB; ++c) {
+          const z_t vc = svp[c];
+          z_t b = sB[c * kBp + r];
+          // b -= tu * conj(vc)
+          b.x -= tu.x * vc.x + tu.y * vc.y;
+          b.y -= tu.y * vc.x - tu.x * vc.y;
+          sB[c * kBp + r] = b;
+        }
+        xr = sB[r];
+      } else {
+        xr = r < L ? a.AB[(1 + r) + s * kLdab] : zero;
+      }
+      // reflector of xr
+      const double xn2 = warp_sum((r >= 1 && r < L) ? zabs2(xr) : 0.0);
+      z_t alpha;
+      alpha.x = __shfl_sync(0xffffffffu, xr.x, 0);
+      alpha.y = __shfl_sync(0xffffffffu, xr.y, 0);
+      double beta;
+      z_t tau, scale;
+      larfg2(alpha, xn2, beta, tau, scale);
+      const z_t v = r == 0 ? one : (r < L ? zmul(scale, xr) : zero);
+      sv[r] = v;
+      a.V2[(int64_t(j) * n + s) * kB + r] = v;
+      if (r == 0) a.tau2[int64_t(j) * n + s] = tau;
+      __syncwarp();
+      if (j == 0) {
+        if (r < L) a.AB[(1 + r) + s * kLdab] = r == 0 ? make_double2(beta, 0.0) : zero;
+        if (r == 0) a.e[s] = beta;
+      } else {
+        // left-apply H^H to Bk columns 1.. (column-wise, lane = column)
+        const int c = r;
+        if (c >= 1) {
+          z_t w = zero;
+          for (int q = 0; q < L; ++q) zcfma(w, sv[q], sB[c * kBp + q]);
+          const z_t tw = zmul(zconj(tau), w);
+          for (int q = 0; q < L; ++q) {
+            z_t b = sB[c * kBp + q];
+            const z_t vq = sv[q];
+            b.x -= vq.x * tw.x - vq.y * tw.y;
+            b.y -= vq.x * tw.y + vq.y * tw.x;
+            sB[c * kBp + q] = b;
+          }
+        } else {
+          sB[0] = make_double2(beta, 0.0);
+          for (int q = 1; q < L; ++q) sB[q] = zero;
+        }
+        __syncwarp();
+        if (r < L)
+          for (int cc = 0; cc < kB; ++cc) a.AB[(kB + r - cc) + (plo + cc) * kLdab] = sB[cc * kBp + r];
+      }
+      // two-sided on D_j: x = tau D v, alpha2 = -1/2 tau x^H v, w = x + alpha2 v
+      z_t xv = zero;
+      for (int c = 0; c < kB; ++c) zfma(xv, sD[c * kBp + r], sv[c]);
+      xv = zmul(tau, xv);
+      const z_t dot = warp_zsum(zcmul(xv, v));
+      const z_t al = zscale(zmul(tau, dot), -0.5);
+      const z_t w = zadd(xv, zmul(al, v));
+      sw[r] = w;
+      __syncwarp();
+      if (r < L) {
+        for (int c = 0; c <= r; ++c) {
+          const z_t vc = sv[c], wc = sw[c];
+          z_t d = sD[c * kBp + r];
+          // d -= v_r conj(w_c) + w_r conj(v_c)
+          d.x -= (v.x * wc.x + v.y * wc.y) + (w.x * vc.x + w.y * vc.y);
+          d.y -= (v.y * wc.x - v.x * wc.y) + (w.y * vc.x - w.x * vc.y);
+          if (c == r) d.y = 0.0;
+          a.AB[(r - c) + (lo + c) * kLdab] = d;
+        }
+      }
+      svp[r] = v;
+      taup = tau;
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release(a.prog + s, j + 1);
+    }
+  }
+}
+
+__global__ void band_diag_kernel(int64_t n, const z_t* __restrict__ AB, double* d) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    d[i] = AB[i * kLdab].x;
+}
+
+// ------------------------------------------------------------------------ back-transform Q2
+struct Q2Args {
+  z_t* Z;
+  int64_t ldz, n, ncols;
+  const z_t* V2;    // [j][s][kB]
+  const z_t* tau2;  // [j][s]
+};
+
+// Z <- Q2 Z. Group (S, j) = reflectors of sweeps s0..s0+31 (s0 = 32 S) at task j, acting on
+// window rows [s0+1+j kB, s0+j kB+64); groups run S descending, j ascending, s descending
+// inside a group. Warp = 8 columns x 4 row residues: lane (rho, col) keeps window rows
+// rho + 4k (k < 16) of its column in registers; reflector i (rows [i, i+31]) is a dot over
+// the lane's rows in range + a 2-step butterfly over rho, then an axpy. Moving to the next
+// group shifts the window 32 rows down: rows k < 8 are stored, k >= 8 move to k - 8, and the
+// new rows are loaded.
+__global__ void __launch_bounds__(32 * kQ2Warps) hb2st_q2_kernel(const __grid_constant__ Q2Args a) {
+  __shared__ z_t vs[32][40];  // v of reflector i at [4 + t], zero padding around
+  __shared__ z_t ts[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rho = lane >> 3, cl = lane & 7;
+  const int64_t col = (int64_t(blockIdx.x) * kQ2Warps + warp) * 8 + cl;
+  const bool cvalid = col < a.ncols;
+  z_t* Zc = a.Z + (cvalid ? col : 0) * a.ldz;
+  const int64_t n = a.n;
+  const z_t zero = make_double2(0.0, 0.0);
+  for (int e = threadIdx.x; e < 32 * 40; e += blockDim.x) (&vs[0][0])[e] = zero;
+  const int nS = int(ceil_div(n - 1, 32));
+  for (int S = nS - 1; S >= 0; --S) {
+    const int64_t s0 = int64_t(S) * 32;
+    const int J = int(ceil_div(n - 1 - s0, kB));  // tasks of sweep s0 (the longest)
+    int64_t wb = s0 + 1;
+    z_t z[kQ2Reg];
+#pragma unroll
+    for (int k = 0; k < kQ2Reg; ++k) {
+      const int64_t row = wb + rho + 4 * k;
+      z[k] = (cvalid && row < n) ? Zc[row] : zero;
+    }
+    for (int j = 0; j < J; ++j) {
+      __syncthreads();  // previous group's vs fully read
+      for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int i = e >> 5, t = e & 31;
+        const int64_t s = s0 + i;
+        z_t v = zero;
+        if (s < n - 1 && j < ceil_div(n - 1 - s, kB)) v = a.V2[(int64_t(j) * n + s) * kB + t];
+        vs[i][4 + t] = v;
+      }
+      if (threadIdx.x < 32) {
+        const int64_t s = s0 + threadIdx.x;
+        ts[threadIdx.x] = (s < n - 1 && j < ceil_div(n - 1 - s, kB)) ? a.tau2[int64_t(j) * n + s]
+                                                                    : zero;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 31; i >= 0; --i) {
+        // window rows [i, i+31]; lane rows rho + 4k: k in [i/4, (i+31)/4] for some rho, the
+        // rows outside the range meet the zero padding of vs
+        const int klo = i / 4;
+        const int khi = min((i + 31) / 4, kQ2Reg - 1);
+        z_t w = zero;
+#pragma unroll
+        for (int k = 0; k < kQ2Reg; ++k)
+          if (k >= klo && k <= khi) zcfma(w, vs[i][4 + rho + 4 * k - i], z[k]);
+        w = zadd(w, shfl_z(w, 8));
+        w = zadd(w, shfl_z(w, 16));
+        const z_t tw = zmul(ts[i], w);
+#pragma unroll
+        for (int k = 0; k < kQ2Reg; ++k)
+          if (k >= klo && k <= khi) {
+            const z_t vk = vs[i][4 + rho + 4 * k - i];
+            z[k].x -= vk.x * tw.x - vk.y * tw.y;
+            z[k].y -= vk.x * tw.y + vk.y * tw.x;
+          }
+      }
+      // shift the window 32 rows down
+#pragma unroll
+      for (int k = 0; k < kQ2Reg / 2; ++k) {
+        const int64_t row = wb + rho + 4 * k;
+        if (cvalid && row < n) Zc[row] = z[k];
+        z[k] = z[k + kQ2Reg / 2];
+        const int64_t nrow = wb + 64 + rho + 4 * k;
+        z[k + kQ2Reg / 2] = (cvalid && nrow < n) ? Zc[nrow] : zero;
+      }
+      wb += 32;
+    }
+#pragma unroll
+    for (int k = 0; k < kQ2Reg; ++k) {
+      const int64_t row = wb + rho + 4 * k;
+      if (cvalid && row < n) Zc[row] = z[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ host side
+namespace {
+struct Ws2 {
+  unsigned* bar;
+  z_t *VW, *WV, *VT, *X, *Y, *T, *alphab, *part, *splitk, *AB, *V2, *tau2;
+  double* normp;
+  int* prog;
+  int64_t nt, splitk_elems;
+};
+
+Ws2 carve(void* ws, int64_t n) {
+  Ws2 w{};
+  char* p = reinterpret_cast<char*>(ws);
+  auto take = [&](size_t bytes) {
+    char* q = p;
+    p += (bytes + 255) & ~size_t(255);
+    return q;
+  };
+  const int64_t G = ceil_div(n, kQrT);
+  w.nt = ceil_div(max64(n - 1, 1), kB);
+  w.splitk_elems = int64_t(16) * kB * kB;
+  w.bar = reinterpret_cast<unsigned*>(take(256));
+  w.VW = reinterpret_cast<z_t*>(take(size_t(n) * 2 * kB * sizeof(z_t)));
+  w.WV = reinterpret_cast<z_t*>(take(size_t(n) * 2 * kB * sizeof(z_t)));
+  w.VT = reinterpret_cast<z_t*>(take(size_t(n) * kB * sizeof(z_t)));
+  w.X = reinterpret_cast<z_t*>(take(size_t(n) * kB * sizeof(z_t)));
+  w.Y = reinterpret_cast<z_t*>(take(size_t(kB) * kB * sizeof(z_t)));
+  w.T = reinterpret_cast<z_t*>(take(size_t(kB) * kB * sizeof(z_t)));
+  w.alphab = reinterpret_cast<z_t*>(take(sizeof(z_t)));
+  w.part = reinterpret_cast<z_t*>(take(size_t(G) * kB * sizeof(z_t)));
+  w.normp = reinterpret_cast<double*>(take(size_t(G) * sizeof(double)));
+  w.splitk = reinterpret_cast<z_t*>(take(size_t(w.splitk_elems) * sizeof(z_t)));
+  w.AB = reinterpret_cast<z_t*>(take(size_t(n) * kLdab * sizeof(z_t)));
+  w.V2 = reinterpret_cast<z_t*>(take(size_t(w.nt) * n * kB * sizeof(z_t)));
+  w.tau2 = reinterpret_cast<z_t*>(take(size_t(w.nt) * n * sizeof(z_t)));
+  w.prog = reinterpret_cast<int*>(take(size_t(n) * sizeof(int)));
+  return w;
+}
+
+size_t chase_smem() { return size_t(kChW) * (2 * kB * kBp + 3 * kB) * sizeof(z_t); }
+}  // namespace
+
+size_t hetrd2_workspace_bytes(int64_t n) {
+  const int64_t G = ceil_div(n, kQrT);
+  const int64_t nt = ceil_div(max64(n - 1, 1), kB);
+  size_t b = 256;
+  b += size_t(n) * kB * 6 * sizeof(z_t);
+  b += size_t(kB) * kB * 2 * sizeof(z_t) + sizeof(z_t);
+  b += size_t(G) * (kB * sizeof(z_t) + sizeof(double));
+  b += size_t(16) * kB * kB * sizeof(z_t);
+  b += size_t(n) * kLdab * sizeof(z_t);
+  b += size_t(nt) * n * (kB + 1) * sizeof(z_t);
+  b += size_t(n) * sizeof(int);
+  return b + 20 * 256;
+}
+
+bool use_two_stage(int64_t n) {
+  static const int env = [] {
+    const char* e = getenv("BSE_TWO_STAGE");
+    return e ? atoi(e) : -1;
+  }();
+  if (n < 4 * kB) return false;
+  if (env >= 0) return env != 0;
+  return false;  // default: one-stage until measured faster
+}
+
+void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, double* e,
+                   z_t* tau1, void* ws) {
+  if (n <= 0) return;
+  Ws2 w = carve(ws, n);
+  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
+  BSE_CUDA(cudaMemsetAsync(tau1, 0, sizeof(z_t) * size_t(n), s));
+  static const bool attr = [] {  // one-time setup (thread-safe: batch lanes)
+    BSE_CUDA(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(chase_smem())));
+    return true;
+  }();
+  (void)attr;
+  // ---- stage 1: panels c0 = 0, kB, ... while the panel has >= 2 rows below the band
+  for (int64_t c0 = 0; c0 + kB <= n - 2; c0 += kB) {
+    const int64_t r0 = c0 + kB, m = n - r0;
+    QrArgs q{};
+    q.P = A + r0 + c0 * lda;
+    q.ldp = lda;
+    q.m = m;
+    q.k = int(min64(m, kB));
+    q.VW = w.VW;
+    q.WV = w.WV;
+    q.VT = w.VT;
+    q.ldw = n;
+    q.T = w.T;
+    q.tau = tau1 + c0;
+    q.normp = w.normp;
+    q.alphab = w.alphab;
+    q.part = w.part;
+    q.bar = w.bar;
+    BSE_CUDA(cudaMemsetAsync(w.bar, 0, 256, s));
+    const int G = int(ceil_div(m, kQrT));
+    void* args[] = {&q};
+    BSE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(he2hb_qr_kernel), dim3(G),
+                                         dim3(kQrT), args, 0, s));
+    count_launch();
+    z_t* A22 = A + r0 + r0 * lda;
+    // X = A22 (V T) over the lower triangle: E (V T) + E^H (V T), E = lower(A22), diagonal
+    // halved (exact power-of-two scaling, restored below)
+    scale_diag(s, m, A22, lda, 0.5);
+    zgemm(s, 0, 0, m, kB, m, one, A22, lda, w.VT, n, zero, w.X, n, kLowerOp, kGeneral, 0,
+          nullptr, 0);
+    zgemm(s, 1, 0, m, kB, m, one, A22, lda, w.VT, n, one, w.X, n, kUpperOp, kGeneral, 0,
+          nullptr, 0);
+    scale_diag(s, m, A22, lda, 2.0);
+    // Y = V^H X ; W = X - 1/2 V T^H Y
+    zgemm(s, 1, 0, kB, kB, m, one, w.VW, n, w.X, n, zero, w.Y, kB, kGeneral, kGeneral, 0,
+          w.splitk, w.splitk_elems);
+    {
+      const int64_t tot = m * kB;
+      he2hb_w_kernel<<<unsigned(ceil_div(tot, 256)), 256, 0, s>>>(m, w.X, w.Y, w.T, w.VW, w.WV,
+                                                                   n);
+      BSE_LAUNCH_CHECK();
+    }
+    // A22 -= V W^H + W V^H (lower tiles)
+    zgemm(s, 0, 1, m, m, 2 * kB, mone, w.VW, n, w.WV, n, one, A22, lda, kGeneral, kGeneral, 1,
+          nullptr, 0);
+  }
+  // ---- stage 2
+  band_pack_kernel<<<unsigned(min64(ceil_div(n * kLdab, 256), 148 * 8)), 256, 0, s>>>(n, A, lda,
+                                                                                     w.AB);
+  BSE_LAUNCH_CHECK();
+  BSE_CUDA(cudaMemsetAsync(w.prog, 0, sizeof(int) * size_t(n), s));
+  {
+    const int64_t nt0 = ceil_div(n - 1, kB);
+    int nw = int(min64(nt0 / 2 + 2, 256));
+    int G = int(ceil_div(nw, kChW));
+    if (g_panel_ctas > 0) G = int(min64(G, max64(g_panel_ctas / 2, 1)));
+    nw = G * kChW;
+    ChaseArgs c{};
+    c.AB = w.AB;
+    c.n = n;
+    c.e = e;
+    c.V2 = w.V2;
+    c.tau2 = w.tau2;
+    c.prog = w.prog;
+    c.nwarps = nw;
+    void* args[] = {&c};
+    BSE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(hb2st_kernel), dim3(G),
+                                         dim3(32 * kChW), args, chase_smem(), s));
+    count_launch();
+  }
+  band_diag_kernel<<<unsigned(min64(ceil_div(n, 256), 148)), 256, 0, s>>>(n, w.AB, d);
+  BSE_LAUNCH_CHECK();
+}
+
+void zunmtr_2stage(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* tau1,
+                   void* ws2, z_t* Z, int64_t ldz, int64_t ncols, void* ws) {
+  if (n <= 1 || ncols <= 0) return;
+  Ws2 w = carve(ws2, n);
+  Q2Args q{};
+  q.Z = Z;
+  q.ldz = ldz;
+  q.n = n;
+  q.ncols = ncols;
+  q.V2 = w.V2;
+  q.tau2 = w.tau2;
+  const int64_t blocks = ceil_div(ncols, 8 * kQ2Warps);
+  hb2st_q2_kernel<<<unsigned(blocks), 32 * kQ2Warps, 0, s>>>(q);
+  BSE_LAUNCH_CHECK();
+  if (n > kB + 1) apply_reflectors(s, 3, n, n - kB, A, lda, tau1, Z, ldz, ncols, ws);
+}
+
+size_t tridiag_workspace_bytes(int64_t n) {
+  return use_two_stage(n) ? hetrd2_workspace_bytes(n) : hetrd_workspace_bytes(n);
+}
+
+void tridiag_reduce(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, double* e,
+                    z_t* tau, void* ws) {
+  if (use_two_stage(n))
+    zhetrd_2stage(s, n, A, lda, d, e, tau, ws);
+  else
+    zhetrd_lower(s, n, A, lda, d, e, tau, ws);
+}
+
+void tridiag_back(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* tau,
+                  void* ws, z_t* Z, int64_t ldz, int64_t ncols, void* ws_unmtr) {
+  if (use_two_stage(n))
+    zunmtr_2stage(s, n, A, lda, tau, ws, Z, ldz, ncols, ws_unmtr);
+  else
+    zunmtr_lower(s, n, A, lda, tau, Z, ldz, ncols, ws_unmtr);
+}
+
+}  // namespace bseg

@@ -127,7 +127,7 @@ size_t solve_workspace_bytes(int method, int64_t n) {
   if (method == BSE_METHOD_CHOL) {
     b += 4 * nn * sizeof(z_t);
     b += stedc_workspace_bytes(n) + nn * sizeof(double);
-    b += hetrd_workspace_bytes(n) + unmtr_workspace_bytes(n, n);
+    b += tridiag_workspace_bytes(n) + unmtr_workspace_bytes(n, n);
     b += trsm_workspace_elems(n, n, 64) * sizeof(z_t);
   } else {
     b += 5 * nn * sizeof(z_t);
@@ -150,7 +150,7 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   z_t* b3 = w.take<z_t>(nn);
   double* Z = w.take<double>(nn);
   void* ws_stedc = w.take<char>(stedc_workspace_bytes(n));
-  void* ws_hetrd = w.take<char>(hetrd_workspace_bytes(n));
+  void* ws_hetrd = w.take<char>(tridiag_workspace_bytes(n));
   void* ws_unmtr = w.take<char>(unmtr_workspace_bytes(n, n));
   z_t* ws_trsm = w.take<z_t>(trsm_workspace_elems(n, n, 64));
   double* d = w.take<double>(n);
@@ -192,7 +192,7 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   herm_lower_sum(s, n, b3, ld, b0, ld);
   clk.mark();
   // hermitian_eig(M) (solvers.cpp:124 -> backend.cpp:34): hetrd + D&C + back-transform
-  zhetrd_lower(s, n, b0, ld, d, e, tau, ws_hetrd);
+  tridiag_reduce(s, n, b0, ld, d, e, tau, ws_hetrd);
   clk.mark();
   dstedc(s, n, d, e, Z, ws_stedc, info + 2);
   {
@@ -210,7 +210,7 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   }
   clk.mark();
   real_to_complex(s, n, n, Z, n, b2, ld);
-  zunmtr_lower(s, n, b0, ld, tau, b2, ld, n, ws_unmtr);
+  tridiag_back(s, n, b0, ld, tau, ws_hetrd, b2, ld, n, ws_unmtr);
   clk.mark();
   // lambda_from_squares (solvers.cpp:125)
   clamp_spectrum(s, n, d, 0, lam, flg, nonpos, counts, floor_p);
