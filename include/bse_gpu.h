@@ -106,6 +106,11 @@ int bse_ctx_set_kernel_timing(bse_ctx* ctx, int enable);
 /* Frees the cached workspace arena (it is otherwise reused across calls). */
 int bse_ctx_release_workspace(bse_ctx* ctx);
 int bse_abi_version(void);
+/* Process-wide choice of the Householder tridiagonalisation inside every Hermitian
+ * eigen-decomposition (zheevd replacement, backend.cpp:34): 0 = one-stage cooperative panels
+ * (default), 1 = two-stage (dense -> band -> tridiagonal, n >= 128). The initial
+ * value comes from the environment variable BSE_TWO_STAGE. Returns the previous mode. */
+int bse_set_tridiagonal_reduction(int mode);
 
 /* ---------------------------------------------------------------- solvers
  * Replace bse::solve_chol (solvers.cpp:119-135), bse::solve_chol_svd (solvers.cpp:137-161)

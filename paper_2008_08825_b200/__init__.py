@@ -285,6 +285,12 @@ class Context:
 _tls = threading.local()
 
 
+def set_tridiagonal_reduction(mode: int) -> int:
+    """Process-wide tridiagonalisation inside every Hermitian eigen-decomposition: 0 one-stage
+    (default), 1 two-stage (n >= 128). Returns the previous mode (bse_set_tridiagonal_reduction)."""
+    return int(_lib.lib().bse_set_tridiagonal_reduction(int(mode)))
+
+
 def default_context(device: int = 0) -> Context:
     ctxs = getattr(_tls, "ctxs", None)
     if ctxs is None:

@@ -613,6 +613,8 @@ int bse_solve_batched_device(bse_ctx* c, int method, int64_t n, int64_t batch,
   });
 }
 
+int bse_set_tridiagonal_reduction(int mode) { return bseg::set_tridiag_mode(mode); }
+
 int bse_ctx_set_batch_lanes(bse_ctx* c, int lanes) {
   if (!c || lanes < 1 || lanes > 8) return BSE_ERR_INVALID_SPEC;
   std::lock_guard<std::mutex> lock(c->mu);

@@ -35,6 +35,7 @@ void zunmtr_2stage(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z
                    void* ws2, z_t* Z, int64_t ldz, int64_t ncols, void* ws);
 // Two-stage reduction for this n in the current mode (batch lanes, or BSE_TWO_STAGE=1/0).
 bool use_two_stage(int64_t n);
+int set_tridiag_mode(int mode);  // bse_set_tridiagonal_reduction; returns the previous mode
 // The eigen-solvers' reduction pair, one- or two-stage per use_two_stage(n) (decided in the
 // calling thread; the same ws must reach tridiag_back).
 size_t tridiag_workspace_bytes(int64_t n);

@@ -24,6 +24,7 @@
 // tools/two_stage_model.py. Every sum has a fixed order: results are bit-deterministic.
 #include <cooperative_groups.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -41,9 +42,9 @@ constexpr int kLdab = 2 * kB;    // packed band: offsets 0 .. 2b-1 below the dia
 constexpr int kChW = 4;          // chase warps per CTA
 constexpr int kBp = kB + 1;      // padded smem block stride
 constexpr int kQ2Rows = 64;      // back-transform window rows (b + 32 - 1, padded)
-constexpr int kQ2Res = 4;        // row residues per column (lanes per column)
+constexpr int kQ2Res = 8;        // row residues per column (lanes per column)
 constexpr int kQ2Reg = kQ2Rows / kQ2Res;  // window rows per thread
-constexpr int kQ2Warps = 4;      // warps per back-transform CTA (8 columns each)
+constexpr int kQ2Warps = 4;      // warps per back-transform CTA (4 columns each)
 
 __device__ __forceinline__ z_t zdiv1(z_t a) {
   const double den = a.x * a.x + a.y * a.y;
@@ -90,12 +91,19 @@ struct QrArgs {
 };
 
 // Householder QR of the m x kB panel (zgeqr2 column order, zlarfg reflectors), V and T
-// (zlarft forward/columnwise) and V T. Thread = panel row, its kB entries in registers.
+// (zlarft forward/columnwise) and V T. Thread = panel row; the CTA's 256 x kB rows live in
+// shared memory (element (r, c) at c * kQrLd + r: a thread walks its row conflict-free).
 // Per column: (1) partial norms + alpha -> grid barrier -> (2) reflector (redundantly per
 // CTA), v, partial w = v^H P(:, c>j) and g = V(:, i<j)^H v in one kB-slot vector ->
 // grid barrier -> (3) totals (fixed order), rank-1 update, T column.
+namespace {
+constexpr int kQrLd = kQrT + 1;
+constexpr size_t kQrSmem = size_t(kB) * kQrLd * sizeof(z_t);
+}  // namespace
 __global__ void __launch_bounds__(kQrT, 1) he2hb_qr_kernel(const __grid_constant__ QrArgs a) {
   GridBarrier grid(a.bar);
+  extern __shared__ __align__(16) unsigned char qsm[];
+  z_t* sP = reinterpret_cast<z_t*>(qsm);
   __shared__ z_t Ts[kB * kB];
   __shared__ z_t wred[kQrT / 32][kB];
   __shared__ z_t wsum[kB];
@@ -107,19 +115,18 @@ __global__ void __launch_bounds__(kQrT, 1) he2hb_qr_kernel(const __grid_constant
   const int64_t r = int64_t(blockIdx.x) * kQrT + tid;
   const bool valid = r < a.m;
   const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
-  z_t p[kB];
-#pragma unroll
-  for (int c = 0; c < kB; ++c) p[c] = valid ? a.P[r + c * a.ldp] : zero;
+  z_t* pr = sP + tid;  // this thread's row: pr[c * kQrLd]
+#pragma unroll 8
+  for (int c = 0; c < kB; ++c) pr[c * kQrLd] = valid ? a.P[r + c * a.ldp] : zero;
   for (int e = tid; e < kB * kB; e += kQrT) Ts[e] = zero;
   if (tid < kB) taus[tid] = zero;
 
-#pragma unroll
-  for (int j = 0; j < kB; ++j) {
-    if (j >= a.k) break;
+  for (int j = 0; j < a.k; ++j) {
     // (1) partial ||P(j+1:, j)||^2 and alpha = P(j, j)
-    const double bs = block_sum((valid && r > j) ? zabs2(p[j]) : 0.0, dred);
+    const z_t pj = pr[j * kQrLd];
+    const double bs = block_sum((valid && r > j) ? zabs2(pj) : 0.0, dred);
     if (tid == 0) a.normp[blockIdx.x] = bs;
-    if (r == j) *a.alphab = p[j];
+    if (r == j) *a.alphab = pj;
     grid.sync();
     // (2) reflector
     if (warp == 0) {
@@ -136,20 +143,16 @@ __global__ void __launch_bounds__(kQrT, 1) he2hb_qr_kernel(const __grid_constant
     z_t tau, scale;
     larfg2(alpha_s, dred[kQrT / 32], beta, tau, scale);
     z_t v = zero;
-    if (valid) v = (r == j) ? one : (r > j ? zmul(scale, p[j]) : zero);
-    if (valid && r > j) p[j] = v;
-    if (r == j) p[j] = make_double2(beta, 0.0);
+    if (valid) v = (r == j) ? one : (r > j ? zmul(scale, pj) : zero);
+    if (valid && r > j) pr[j * kQrLd] = v;
+    if (r == j) pr[j * kQrLd] = make_double2(beta, 0.0);
     // slot c > j: conj(v) P(r, c); slot i < j: conj(V(r, i)) v ; slot j: 0
     z_t sl[16], sh[16];
 #pragma unroll
     for (int c = 0; c < kB; ++c) {
-      z_t t = zero;
-      if (c > j) {
-        t = zcmul(v, p[c]);
-      } else if (c < j) {
-        const z_t vi = r > c ? p[c] : (r == c ? one : zero);
-        t = zcmul(vi, v);
-      }
+      const z_t pc = pr[c * kQrLd];
+      const z_t vi = r > c ? pc : (r == c ? one : zero);
+      const z_t t = c > j ? zcmul(v, pc) : (c < j ? zcmul(vi, v) : zero);
       if (c < 16) sl[c] = t; else sh[c - 16] = t;
     }
     __syncthreads();  // re-converge before the butterflies
@@ -167,16 +170,23 @@ __global__ void __launch_bounds__(kQrT, 1) he2hb_qr_kernel(const __grid_constant
       a.part[int64_t(blockIdx.x) * kB + tid] = t;
     }
     grid.sync();
-    // (3) totals, update, T(:, j)
-    if (tid < kB) {
+    // (3) totals (warp w sums CTAs w, w+8, ...; then a fixed-order sum over the warps), update,
+    // T(:, j)
+    {
       z_t t = zero;
-      for (int g = 0; g < G; ++g) t = zadd(t, a.part[int64_t(g) * kB + tid]);
+      for (int g = warp; g < G; g += kQrT / 32) t = zadd(t, a.part[int64_t(g) * kB + lane]);
+      wred[warp][lane] = t;
+    }
+    __syncthreads();
+    if (tid < kB) {
+      z_t t = wred[0][tid];
+#pragma unroll
+      for (int w = 1; w < kQrT / 32; ++w) t = zadd(t, wred[w][tid]);
       wsum[tid] = t;
     }
     __syncthreads();
-    const z_t ct = zconj(tau);
-#pragma unroll
-    for (int c = j + 1; c < kB; ++c) p[c] = zsub(p[c], zmul(zmul(ct, v), wsum[c]));
+    const z_t cv = zmul(zconj(tau), v);
+    for (int c = j + 1; c < kB; ++c) pr[c * kQrLd] = zsub(pr[c * kQrLd], zmul(cv, wsum[c]));
     if (tid < kB) {
       z_t t = zero;
       if (tid < j) {  // T(i, j) = -tau sum_{i' = i}^{j-1} T(i, i') g(i')
@@ -191,12 +201,12 @@ __global__ void __launch_bounds__(kQrT, 1) he2hb_qr_kernel(const __grid_constant
   }
   __syncthreads();
   if (valid) {
-#pragma unroll
-    for (int c = 0; c < kB; ++c) a.P[r + c * a.ldp] = p[c];
     z_t vx[kB];
 #pragma unroll
     for (int c = 0; c < kB; ++c) {
-      vx[c] = c < a.k ? (r > c ? p[c] : (r == c ? one : zero)) : zero;
+      const z_t pc = pr[c * kQrLd];
+      a.P[r + c * a.ldp] = pc;
+      vx[c] = c < a.k ? (r > c ? pc : (r == c ? one : zero)) : zero;
       a.VW[r + c * a.ldw] = vx[c];
       a.WV[r + (kB + c) * a.ldw] = vx[c];
     }
@@ -266,8 +276,7 @@ struct ChaseArgs {
   double* e;      // e[s] = beta of task (s, 0)
   z_t* V2;        // [j][s][kB] reflectors (v[0] = 1), zero padded
   z_t* tau2;      // [j][s]
-  int* prog;      // tasks finished per sweep (zeroed)
-  int nwarps;
+  int* prog;      // tasks finished per sweep (zeroed; published for each group's last sweep)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -279,10 +288,14 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Bulge chasing, one warp per sweep (sweeps round-robin over the warps of a cooperative grid,
-// so every sweep a warp waits on is owned by a resident warp). Lane r owns row r of the
-// 32x32 blocks for row-wise products and column r for column-wise ones; sB / sD are the bulge
-// block Bk_j and the (Hermitian-expanded) diagonal block D_j.
+// Bulge chasing. A CTA takes groups of kChW consecutive sweeps (groups dealt round-robin over
+// a cooperative grid) and runs each group as a wavefront: at step t warp w does task
+// j = t - 2w of sweep sb + w, and one CTA barrier per step orders the warps (task j of sweep s
+// needs task j+1 of sweep s-1, done by warp w-1 a step earlier; the two tasks running side by
+// side touch disjoint entries). The group's first sweep waits on the previous group's last
+// sweep through its progress counter (acquire/release). Per task the 32x32 blocks are staged
+// with cp.async (one round trip), lane r owning row r for row-wise products and column r for
+// column-wise ones; sB / sD hold the bulge block Bk_j and the Hermitian-expanded D_j.
 __global__ void __launch_bounds__(32 * kChW, 1) hb2st_kernel(const __grid_constant__ ChaseArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,54 +304,67 @@ __global__ void __launch_bounds__(32 * kChW, 1) hb2st_kernel(const __grid_consta
   z_t* sv = sD + kB * kBp;  // current reflector
   z_t* sw = sv + kB;        // two-sided w
   z_t* svp = sw + kB;       // previous reflector of the sweep
-  const int64_t n = a.n;
+  const int64_t n = a.n, nsw = n - 1;
   const z_t zero = make_double2(0.0, 0.0), one = make_double2(1.0, 0.0);
-  const int gw = blockIdx.x * kChW + warp;
-  for (int64_t s = gw; s < n - 1; s += a.nwarps) {
-    const int nt = int(ceil_div(n - 1 - s, kB));
-    const int ntp = s > 0 ? int(ceil_div(n - s, kB)) : 0;  // tasks of sweep s-1
+  const int r = lane;
+  for (int64_t g = blockIdx.x; g * kChW < nsw; g += gridDim.x) {
+    const int64_t sb = g * kChW, s = sb + warp;
+    const int nt = s < nsw ? int(ceil_div(nsw - s, kB)) : 0;
+    const int nt0 = int(ceil_div(nsw - sb, kB));
+    const int ntp = sb > 0 ? int(ceil_div(nsw - sb + 1, kB)) : 0;  // tasks of sweep sb - 1
+    const int steps = nt0 + 2 * (kChW - 1);
     z_t taup = zero;
-    for (int j = 0; j < nt; ++j) {
-      if (s > 0) {
-        const int need = min(j + 2, ntp);
-        while (ld_acquire(a.prog + s - 1) < need) {
+    for (int t = 0; t < steps; ++t) {
+      if (warp == 0 && sb > 0 && t < nt0) {
+        const int need = min(t + 2, ntp);
+        while (ld_acquire(a.prog + sb - 1) < need) {
         }
       }
-      __syncwarp();
+      __syncthreads();
+      const int j = t - 2 * warp;
+      if (j < 0 || j >= nt) continue;
       const int64_t lo = s + 1 + int64_t(j) * kB;
       const int L = int(min64(kB, n - lo));
-      const int r = lane;
-      // D_j (Hermitian expanded, zero outside L x L)
-      for (int c = 0; c < kB; ++c) {
-        z_t x = zero;
-        if (c < L && r >= c && r < L) x = a.AB[(r - c) + (lo + c) * kLdab];
-        if (r == c) x.y = 0.0;
-        if (r >= c) sD[c * kBp + r] = x;  // each element written once (lower by its row's
-        if (r > c) sD[r * kBp + c] = zconj(x);  // lane, the mirror by the column's lane)
-      }
-      z_t xr;  // column to annihilate (row r)
       const int64_t plo = lo - kB;
+      // ---- stage D_j (lower, zero outside L x L) and Bk_j in one round trip
+#pragma unroll 8
+      for (int c = 0; c < kB; ++c) {
+        const bool okd = c < L && r >= c && r < L;
+        if (r >= c) cp_async16(sD + c * kBp + r, okd ? a.AB + (r - c) + (lo + c) * kLdab : a.AB, okd);
+      }
       if (j > 0) {
-        for (int c = 0; c < kB; ++c)
-          sB[c * kBp + r] = r < L ? a.AB[(kB + r - c) + (plo + c) * kLdab] : zero;
-        __syncwarp();
-        // right-apply the previous reflector: Bk -= taup (Bk vp) vp^H (row-wise, lane = row)
+#pragma unroll 8
+        for (int c = 0; c < kB; ++c) {
+          const bool okb = r < L;
+          cp_async16(sB + c * kBp + r, okb ? a.AB + (kB + r - c) + (plo + c) * kLdab : a.AB, okb);
+        }
+      }
+      z_t xr = zero;
+      if (j == 0 && r < L) xr = a.AB[(1 + r) + s * kLdab];
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+      {  // mirror of D (row r's lane writes the upper entries of column r), real diagonal
+        sD[r * kBp + r].y = 0.0;
+        for (int c = 0; c < r; ++c) sD[r * kBp + c] = zconj(sD[c * kBp + r]);
+      }
+      if (j > 0) {
+        // right-apply the previous reflector: Bk -= taup (Bk vp) vp^H (lane = row)
         z_t u = zero;
+#pragma unroll 8
         for (int c = 0; c < kB; ++c) zfma(u, sB[c * kBp + r], svp[c]);
         const z_t tu = zmul(taup, u);
+#pragma unroll 8
         for (int c = 0; c < kB; ++c) {
           const z_t vc = svp[c];
           z_t b = sB[c * kBp + r];
-          // b -= tu * conj(vc)
-          b.x -= tu.x * vc.x + tu.y * vc.y;
+          b.x -= tu.x * vc.x + tu.y * vc.y;  // b -= tu conj(vc)
           b.y -= tu.y * vc.x - tu.x * vc.y;
           sB[c * kBp + r] = b;
         }
         xr = sB[r];
-      } else {
-        xr = r < L ? a.AB[(1 + r) + s * kLdab] : zero;
       }
-      // reflector of xr
+      // ---- reflector of the column (rows lo .. lo+L-1)
       const double xn2 = warp_sum((r >= 1 && r < L) ? zabs2(xr) : 0.0);
       z_t alpha;
       alpha.x = __shfl_sync(0xffffffffu, xr.x, 0);
@@ -355,7 +381,7 @@ __global__ void __launch_bounds__(32 * kChW, 1) hb2st_kernel(const __grid_consta
         if (r < L) a.AB[(1 + r) + s * kLdab] = r == 0 ? make_double2(beta, 0.0) : zero;
         if (r == 0) a.e[s] = beta;
       } else {
-        // left-apply H^H to Bk columns 1.. (column-wise, lane = column)
+        // left-apply H^H to Bk columns 1.. (lane = column); column 0 becomes (beta, 0, ...)
         const int c = r;
         if (c >= 1) {
           z_t w = zero;
@@ -373,11 +399,15 @@ __global__ void __launch_bounds__(32 * kChW, 1) hb2st_kernel(const __grid_consta
           for (int q = 1; q < L; ++q) sB[q] = zero;
         }
         __syncwarp();
-        if (r < L)
-          for (int cc = 0; cc < kB; ++cc) a.AB[(kB + r - cc) + (plo + cc) * kLdab] = sB[cc * kBp + r];
+        if (r < L) {
+#pragma unroll 8
+          for (int cc = 0; cc < kB; ++cc)
+            a.AB[(kB + r - cc) + (plo + cc) * kLdab] = sB[cc * kBp + r];
+        }
       }
-      // two-sided on D_j: x = tau D v, alpha2 = -1/2 tau x^H v, w = x + alpha2 v
+      // ---- two-sided on D_j: x = tau D v, alpha2 = -1/2 tau x^H v, w = x + alpha2 v
       z_t xv = zero;
+#pragma unroll 8
       for (int c = 0; c < kB; ++c) zfma(xv, sD[c * kBp + r], sv[c]);
       xv = zmul(tau, xv);
       const z_t dot = warp_zsum(zcmul(xv, v));
@@ -398,10 +428,13 @@ __global__ void __launch_bounds__(32 * kChW, 1) hb2st_kernel(const __grid_consta
       }
       svp[r] = v;
       taup = tau;
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release(a.prog + s, j + 1);
+      if (warp == kChW - 1) {  // the next group's first sweep waits on this one
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(a.prog + s, j + 1);
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -421,85 +454,117 @@ struct Q2Args {
 
 // Z <- Q2 Z. Group (S, j) = reflectors of sweeps s0..s0+31 (s0 = 32 S) at task j, acting on
 // window rows [s0+1+j kB, s0+j kB+64); groups run S descending, j ascending, s descending
-// inside a group. Warp = 8 columns x 4 row residues: lane (rho, col) keeps window rows
-// rho + 4k (k < 16) of its column in registers; reflector i (rows [i, i+31]) is a dot over
-// the lane's rows in range + a 2-step butterfly over rho, then an axpy. Moving to the next
-// group shifts the window 32 rows down: rows k < 8 are stored, k >= 8 move to k - 8, and the
-// new rows are loaded.
+// inside a group (tools/two_stage_model.py). Warp = 4 columns x 8 row residues: lane
+// (rho, col) keeps window rows rho + 8k (k < 8) of its column in registers; reflector i
+// (rows [i, i+31]) is a dot over the lane's rows in range (the others meet the zero padding
+// of vs), a 3-step butterfly over rho and an axpy. The next group's reflectors stream into
+// the other shared buffer (cp.async) while a group computes. Between groups of a pass the
+// window moves 32 rows down: rows k < 4 are stored, k >= 4 move to k - 4, new rows load.
+namespace {
+constexpr int kVsW = 46;  // padded reflector row: v(t) at [7 + t], zeros at [0, 7) and [39, 46)
+__device__ __forceinline__ bool q2_valid(int64_t s, int j, int64_t n) {
+  return s < n - 1 && j < ceil_div(n - 1 - s, kB);
+}
+}  // namespace
+
 __global__ void __launch_bounds__(32 * kQ2Warps) hb2st_q2_kernel(const __grid_constant__ Q2Args a) {
-  __shared__ z_t vs[32][40];  // v of reflector i at [4 + t], zero padding around
-  __shared__ z_t ts[32];
+  __shared__ __align__(16) z_t vs[2][32][kVsW];
+  __shared__ __align__(16) z_t ts[2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rho = lane >> 3, cl = lane & 7;
-  const int64_t col = (int64_t(blockIdx.x) * kQ2Warps + warp) * 8 + cl;
+  const int rho = lane >> 2, cl = lane & 3;
+  const int64_t col = (int64_t(blockIdx.x) * kQ2Warps + warp) * 4 + cl;
   const bool cvalid = col < a.ncols;
   z_t* Zc = a.Z + (cvalid ? col : 0) * a.ldz;
   const int64_t n = a.n;
   const z_t zero = make_double2(0.0, 0.0);
-  for (int e = threadIdx.x; e < 32 * 40; e += blockDim.x) (&vs[0][0])[e] = zero;
-  const int nS = int(ceil_div(n - 1, 32));
-  for (int S = nS - 1; S >= 0; --S) {
+  for (int e = threadIdx.x; e < 2 * 32 * kVsW; e += blockDim.x) (&vs[0][0][0])[e] = zero;
+  __syncthreads();
+  auto prefetch = [&](int buf, int S, int j) {
     const int64_t s0 = int64_t(S) * 32;
-    const int J = int(ceil_div(n - 1 - s0, kB));  // tasks of sweep s0 (the longest)
-    int64_t wb = s0 + 1;
-    z_t z[kQ2Reg];
-#pragma unroll
-    for (int k = 0; k < kQ2Reg; ++k) {
-      const int64_t row = wb + rho + 4 * k;
-      z[k] = (cvalid && row < n) ? Zc[row] : zero;
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+      const int i = e >> 5, t = e & 31;
+      const bool ok = q2_valid(s0 + i, j, n);
+      cp_async16(&vs[buf][i][7 + t], ok ? a.V2 + (int64_t(j) * n + s0 + i) * kB + t : a.V2, ok);
     }
-    for (int j = 0; j < J; ++j) {
-      __syncthreads();  // previous group's vs fully read
-      for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-        const int i = e >> 5, t = e & 31;
-        const int64_t s = s0 + i;
-        z_t v = zero;
-        if (s < n - 1 && j < ceil_div(n - 1 - s, kB)) v = a.V2[(int64_t(j) * n + s) * kB + t];
-        vs[i][4 + t] = v;
-      }
-      if (threadIdx.x < 32) {
-        const int64_t s = s0 + threadIdx.x;
-        ts[threadIdx.x] = (s < n - 1 && j < ceil_div(n - 1 - s, kB)) ? a.tau2[int64_t(j) * n + s]
-                                                                    : zero;
-      }
-      __syncthreads();
+    if (threadIdx.x < 32) {
+      const bool ok = q2_valid(s0 + threadIdx.x, j, n);
+      cp_async16(&ts[buf][threadIdx.x], ok ? a.tau2 + int64_t(j) * n + s0 + threadIdx.x : a.tau2,
+                 ok);
+    }
+  };
+  auto tasks = [&](int S) { return int(ceil_div(n - 1 - int64_t(S) * 32, kB)); };
+  const int nS = int(ceil_div(n - 1, 32));
+  int S = nS - 1, j = 0, buf = 0;
+  int64_t wb = int64_t(S) * 32 + 1;
+  z_t z[kQ2Reg];
 #pragma unroll
-      for (int i = 31; i >= 0; --i) {
-        // window rows [i, i+31]; lane rows rho + 4k: k in [i/4, (i+31)/4] for some rho, the
-        // rows outside the range meet the zero padding of vs
-        const int klo = i / 4;
-        const int khi = min((i + 31) / 4, kQ2Reg - 1);
-        z_t w = zero;
+  for (int k = 0; k < kQ2Reg; ++k) {
+    const int64_t row = wb + rho + 8 * k;
+    z[k] = (cvalid && row < n) ? Zc[row] : zero;
+  }
+  prefetch(0, S, 0);
+  cp_async_commit();
+  while (S >= 0) {
+    const bool same = j + 1 < tasks(S);
+    const int S2 = same ? S : S - 1, j2 = same ? j + 1 : 0;
+    if (S2 >= 0) prefetch(buf ^ 1, S2, j2);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kQ2Reg; ++k)
-          if (k >= klo && k <= khi) zcfma(w, vs[i][4 + rho + 4 * k - i], z[k]);
-        w = zadd(w, shfl_z(w, 8));
-        w = zadd(w, shfl_z(w, 16));
-        const z_t tw = zmul(ts[i], w);
+    for (int i = 31; i >= 0; --i) {
+      const int klo = i / 8, khi = min((i + 31) / 8, kQ2Reg - 1);
+      z_t w0 = zero, w1 = zero;
 #pragma unroll
-        for (int k = 0; k < kQ2Reg; ++k)
-          if (k >= klo && k <= khi) {
-            const z_t vk = vs[i][4 + rho + 4 * k - i];
-            z[k].x -= vk.x * tw.x - vk.y * tw.y;
-            z[k].y -= vk.x * tw.y + vk.y * tw.x;
-          }
-      }
-      // shift the window 32 rows down
+      for (int k = 0; k < kQ2Reg; ++k)
+        if (k >= klo && k <= khi) {
+          if (k & 1)
+            zcfma(w1, vs[buf][i][7 + rho + 8 * k - i], z[k]);
+          else
+            zcfma(w0, vs[buf][i][7 + rho + 8 * k - i], z[k]);
+        }
+      z_t w = zadd(w0, w1);
+      w = zadd(w, shfl_z(w, 4));
+      w = zadd(w, shfl_z(w, 8));
+      w = zadd(w, shfl_z(w, 16));
+      const z_t tw = zmul(ts[buf][i], w);
+#pragma unroll
+      for (int k = 0; k < kQ2Reg; ++k)
+        if (k >= klo && k <= khi) {
+          const z_t vk = vs[buf][i][7 + rho + 8 * k - i];
+          z[k].x -= vk.x * tw.x - vk.y * tw.y;
+          z[k].y -= vk.x * tw.y + vk.y * tw.x;
+        }
+    }
+    __syncthreads();  // vs[buf] is refilled by the next iteration's prefetch
+    if (same) {  // window 32 rows down
 #pragma unroll
       for (int k = 0; k < kQ2Reg / 2; ++k) {
-        const int64_t row = wb + rho + 4 * k;
+        const int64_t row = wb + rho + 8 * k;
         if (cvalid && row < n) Zc[row] = z[k];
         z[k] = z[k + kQ2Reg / 2];
-        const int64_t nrow = wb + 64 + rho + 4 * k;
+        const int64_t nrow = wb + 64 + rho + 8 * k;
         z[k + kQ2Reg / 2] = (cvalid && nrow < n) ? Zc[nrow] : zero;
       }
       wb += 32;
-    }
+    } else {  // pass done: store the window, load the next pass's first window
 #pragma unroll
-    for (int k = 0; k < kQ2Reg; ++k) {
-      const int64_t row = wb + rho + 4 * k;
-      if (cvalid && row < n) Zc[row] = z[k];
+      for (int k = 0; k < kQ2Reg; ++k) {
+        const int64_t row = wb + rho + 8 * k;
+        if (cvalid && row < n) Zc[row] = z[k];
+      }
+      if (S2 >= 0) {
+        wb = int64_t(S2) * 32 + 1;
+#pragma unroll
+        for (int k = 0; k < kQ2Reg; ++k) {
+          const int64_t row = wb + rho + 8 * k;
+          z[k] = (cvalid && row < n) ? Zc[row] : zero;
+        }
+      }
     }
+    S = S2;
+    j = j2;
+    buf ^= 1;
   }
 }
 
@@ -507,10 +572,10 @@ __global__ void __launch_bounds__(32 * kQ2Warps) hb2st_q2_kernel(const __grid_co
 namespace {
 struct Ws2 {
   unsigned* bar;
-  z_t *VW, *WV, *VT, *X, *Y, *T, *alphab, *part, *splitk, *AB, *V2, *tau2;
+  z_t *VW, *WV, *VT, *X, *Y, *T, *alphab, *part, *splitk, *hsplit, *AB, *V2, *tau2;
   double* normp;
   int* prog;
-  int64_t nt, splitk_elems;
+  int64_t nt, splitk_elems, hsplit_elems;
 };
 
 Ws2 carve(void* ws, int64_t n) {
@@ -535,6 +600,8 @@ Ws2 carve(void* ws, int64_t n) {
   w.part = reinterpret_cast<z_t*>(take(size_t(G) * kB * sizeof(z_t)));
   w.normp = reinterpret_cast<double*>(take(size_t(G) * sizeof(double)));
   w.splitk = reinterpret_cast<z_t*>(take(size_t(w.splitk_elems) * sizeof(z_t)));
+  w.hsplit_elems = int64_t(16) * n * kB;
+  w.hsplit = reinterpret_cast<z_t*>(take(size_t(w.hsplit_elems) * sizeof(z_t)));
   w.AB = reinterpret_cast<z_t*>(take(size_t(n) * kLdab * sizeof(z_t)));
   w.V2 = reinterpret_cast<z_t*>(take(size_t(w.nt) * n * kB * sizeof(z_t)));
   w.tau2 = reinterpret_cast<z_t*>(take(size_t(w.nt) * n * sizeof(z_t)));
@@ -553,21 +620,24 @@ size_t hetrd2_workspace_bytes(int64_t n) {
   b += size_t(kB) * kB * 2 * sizeof(z_t) + sizeof(z_t);
   b += size_t(G) * (kB * sizeof(z_t) + sizeof(double));
   b += size_t(16) * kB * kB * sizeof(z_t);
+  b += size_t(16) * n * kB * sizeof(z_t);
   b += size_t(n) * kLdab * sizeof(z_t);
   b += size_t(nt) * n * (kB + 1) * sizeof(z_t);
   b += size_t(n) * sizeof(int);
   return b + 20 * 256;
 }
 
-bool use_two_stage(int64_t n) {
-  static const int env = [] {
-    const char* e = getenv("BSE_TWO_STAGE");
-    return e ? atoi(e) : -1;
-  }();
-  if (n < 4 * kB) return false;
-  if (env >= 0) return env != 0;
-  return false;  // default: one-stage until measured faster
-}
+namespace {
+// 0 = one-stage (default: measured faster on B200), 1 = two-stage
+std::atomic<int> g_tridiag_mode{[] {
+  const char* e = getenv("BSE_TWO_STAGE");
+  return e && atoi(e) != 0 ? 1 : 0;
+}()};
+}  // namespace
+
+int set_tridiag_mode(int mode) { return g_tridiag_mode.exchange(mode != 0 ? 1 : 0); }
+
+bool use_two_stage(int64_t n) { return n >= 4 * kB && g_tridiag_mode.load() != 0; }
 
 void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, double* e,
                    z_t* tau1, void* ws) {
@@ -578,6 +648,8 @@ void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, do
   static const bool attr = [] {  // one-time setup (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(chase_smem())));
+    BSE_CUDA(cudaFuncSetAttribute(he2hb_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kQrSmem)));
     return true;
   }();
   (void)attr;
@@ -603,16 +675,16 @@ void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, do
     const int G = int(ceil_div(m, kQrT));
     void* args[] = {&q};
     BSE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(he2hb_qr_kernel), dim3(G),
-                                         dim3(kQrT), args, 0, s));
+                                         dim3(kQrT), args, kQrSmem, s));
     count_launch();
     z_t* A22 = A + r0 + r0 * lda;
     // X = A22 (V T) over the lower triangle: E (V T) + E^H (V T), E = lower(A22), diagonal
     // halved (exact power-of-two scaling, restored below)
     scale_diag(s, m, A22, lda, 0.5);
     zgemm(s, 0, 0, m, kB, m, one, A22, lda, w.VT, n, zero, w.X, n, kLowerOp, kGeneral, 0,
-          nullptr, 0);
+          w.hsplit, w.hsplit_elems);
     zgemm(s, 1, 0, m, kB, m, one, A22, lda, w.VT, n, one, w.X, n, kUpperOp, kGeneral, 0,
-          nullptr, 0);
+          w.hsplit, w.hsplit_elems);
     scale_diag(s, m, A22, lda, 2.0);
     // Y = V^H X ; W = X - 1/2 V T^H Y
     zgemm(s, 1, 0, kB, kB, m, one, w.VW, n, w.X, n, zero, w.Y, kB, kGeneral, kGeneral, 0,
@@ -634,10 +706,8 @@ void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, do
   BSE_CUDA(cudaMemsetAsync(w.prog, 0, sizeof(int) * size_t(n), s));
   {
     const int64_t nt0 = ceil_div(n - 1, kB);
-    int nw = int(min64(nt0 / 2 + 2, 256));
-    int G = int(ceil_div(nw, kChW));
+    int G = int(min64(ceil_div(nt0, 2 * kChW) + 2, 148));
     if (g_panel_ctas > 0) G = int(min64(G, max64(g_panel_ctas / 2, 1)));
-    nw = G * kChW;
     ChaseArgs c{};
     c.AB = w.AB;
     c.n = n;
@@ -645,7 +715,6 @@ void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, do
     c.V2 = w.V2;
     c.tau2 = w.tau2;
     c.prog = w.prog;
-    c.nwarps = nw;
     void* args[] = {&c};
     BSE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(hb2st_kernel), dim3(G),
                                          dim3(32 * kChW), args, chase_smem(), s));
@@ -666,7 +735,7 @@ void zunmtr_2stage(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z
   q.ncols = ncols;
   q.V2 = w.V2;
   q.tau2 = w.tau2;
-  const int64_t blocks = ceil_div(ncols, 8 * kQ2Warps);
+  const int64_t blocks = ceil_div(ncols, 4 * kQ2Warps);
   hb2st_q2_kernel<<<unsigned(blocks), 32 * kQ2Warps, 0, s>>>(q);
   BSE_LAUNCH_CHECK();
   if (n > kB + 1) apply_reflectors(s, 3, n, n - kB, A, lda, tau1, Z, ldz, ncols, ws);
