@@ -531,6 +531,11 @@ void run_batch(bse_ctx* c, const BatchIO& io, int64_t batch, int64_t* failed_ind
   BSE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const int prev_cap = g_panel_ctas;
   g_panel_ctas = lanes > 1 ? sms / lanes : 0;
+  static const int cap_env = [] {  // developer A/B switch: panel CTAs per lane
+    const char* e = getenv("BSE_PANEL_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (lanes > 1 && cap_env > 0) g_panel_ctas = cap_env;
   struct Restore {
     int v;
     ~Restore() { g_panel_ctas = v; }
