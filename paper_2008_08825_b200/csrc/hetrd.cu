@@ -712,21 +712,18 @@ size_t unmtr_workspace_bytes(int64_t n, int64_t ncols) {
 
 // Z <- H(0) H(1) ... H(nref-1) Z for the reflector family `mode`, applied in kBT-blocks from
 // the last to the first as Z <- Z - (V T)(V^H Z). V, T and V T of all blocks are formed up
-// front (batched), so the serial part per block is just two DMMA GEMMs.
-void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z_t* A,
-                      int64_t lda, const z_t* tau, z_t* Z, int64_t ldz, int64_t ncols, void* ws) {
-  if (nref <= 0 || ncols <= 0) return;
-  const int off = reflector_offset(mode);
+// front (batched, prepare_reflectors: needs only the reflectors, so the solvers run it on the
+// aux stream beside the divide & conquer), and the serial part per block is two DMMA GEMMs.
+void prepare_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z_t* A,
+                        int64_t lda, const z_t* tau, void* ws) {
+  if (nref <= 0) return;
   const int64_t nblk = ceil_div(nref, kBT);
   const int64_t ncol = nblk * kBT;
   z_t* Vall = reinterpret_cast<z_t*>(ws);
   z_t* VTall = Vall + n * ncol;
   z_t* Gall = VTall + n * ncol;
   z_t* Tall = Gall + nblk * kBT * kBT;
-  z_t* W1 = Tall + nblk * kBT * kBT;
-  z_t* part = W1 + int64_t(kBT) * ncols;
-  const int64_t part_elems = int64_t(16) * kBT * ncols;
-  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
+  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0};
   {
     const int blocks = int(min64(ceil_div(n * ncol, 256), 148 * 16));
     build_vall_kernel<<<blocks, 256, 0, s>>>(A, lda, n, nref, ncol, mode, Vall);
@@ -740,6 +737,22 @@ void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z
   // (V T)_b, all blocks in one launch
   zgemm_batched(s, 0, 0, n, kBT, kBT, one, Vall, n, n * kBT, Tall, kBT, int64_t(kBT) * kBT, zero,
                 VTall, n, n * kBT, int(nblk));
+}
+
+void apply_prepared_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, z_t* Z,
+                               int64_t ldz, int64_t ncols, void* ws) {
+  if (nref <= 0 || ncols <= 0) return;
+  const int off = reflector_offset(mode);
+  const int64_t nblk = ceil_div(nref, kBT);
+  const int64_t ncol = nblk * kBT;
+  z_t* Vall = reinterpret_cast<z_t*>(ws);
+  z_t* VTall = Vall + n * ncol;
+  z_t* Gall = VTall + n * ncol;
+  z_t* Tall = Gall + nblk * kBT * kBT;
+  z_t* W1 = Tall + nblk * kBT * kBT;
+  z_t* part = W1 + int64_t(kBT) * ncols;
+  const int64_t part_elems = int64_t(16) * kBT * ncols;
+  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
   for (int64_t b = nblk - 1; b >= 0; --b) {
     const int64_t j0 = b * kBT;
     const int64_t r0 = j0 + off;  // first row any reflector of the block touches
@@ -755,6 +768,13 @@ void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z
     zgemm(s, 0, 0, m, ncols, kBT, mone, VTb, n, W1, kBT, one, Zb, ldz, kGeneral, kGeneral, 0,
           nullptr, 0);
   }
+}
+
+void apply_reflectors(cudaStream_t s, int mode, int64_t n, int64_t nref, const z_t* A,
+                      int64_t lda, const z_t* tau, z_t* Z, int64_t ldz, int64_t ncols, void* ws) {
+  if (nref <= 0 || ncols <= 0) return;
+  prepare_reflectors(s, mode, n, nref, A, lda, tau, ws);
+  apply_prepared_reflectors(s, mode, n, nref, Z, ldz, ncols, ws);
 }
 
 void zunmtr_lower(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* tau, z_t* Z,

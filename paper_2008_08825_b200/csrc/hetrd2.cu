@@ -738,7 +738,7 @@ void zunmtr_2stage(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z
   const int64_t blocks = ceil_div(ncols, 4 * kQ2Warps);
   hb2st_q2_kernel<<<unsigned(blocks), 32 * kQ2Warps, 0, s>>>(q);
   BSE_LAUNCH_CHECK();
-  if (n > kB + 1) apply_reflectors(s, 3, n, n - kB, A, lda, tau1, Z, ldz, ncols, ws);
+  if (n > kB + 1) apply_prepared_reflectors(s, 3, n, n - kB, Z, ldz, ncols, ws);  // Q1
 }
 
 size_t tridiag_workspace_bytes(int64_t n) {
@@ -753,12 +753,23 @@ void tridiag_reduce(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, d
     zhetrd_lower(s, n, A, lda, d, e, tau, ws);
 }
 
+void tridiag_back_prepare(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* tau,
+                          void* ws_unmtr) {
+  if (use_two_stage(n)) {
+    if (n > kB + 1) prepare_reflectors(s, 3, n, n - kB, A, lda, tau, ws_unmtr);
+  } else {
+    prepare_reflectors(s, 0, n, n - 1, A, lda, tau, ws_unmtr);
+  }
+}
+
 void tridiag_back(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z_t* tau,
-                  void* ws, z_t* Z, int64_t ldz, int64_t ncols, void* ws_unmtr) {
-  if (use_two_stage(n))
+                  void* ws, z_t* Z, int64_t ldz, int64_t ncols, void* ws_unmtr, bool prepared) {
+  if (!prepared) tridiag_back_prepare(s, n, A, lda, tau, ws_unmtr);
+  if (use_two_stage(n)) {
     zunmtr_2stage(s, n, A, lda, tau, ws, Z, ldz, ncols, ws_unmtr);
-  else
-    zunmtr_lower(s, n, A, lda, tau, Z, ldz, ncols, ws_unmtr);
+  } else {
+    apply_prepared_reflectors(s, 0, n, n - 1, Z, ldz, ncols, ws_unmtr);
+  }
 }
 
 }  // namespace bseg

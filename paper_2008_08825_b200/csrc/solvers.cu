@@ -194,7 +194,12 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   // hermitian_eig(M) (solvers.cpp:124 -> backend.cpp:34): hetrd + D&C + back-transform
   tridiag_reduce(s, n, b0, ld, d, e, tau, ws_hetrd);
   clk.mark();
+  // the back-transform's reflector blocks need only the reduction: built on the aux stream
+  // while the divide & conquer runs (joined before the host sync below)
+  fork(c);
+  tridiag_back_prepare(c->aux, n, b0, ld, tau, ws_unmtr);
   dstedc(s, n, d, e, Z, ws_stedc, info + 2);
+  join(c);
   {
     int h = 0;
     double dmin = 0.0;
@@ -210,7 +215,7 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   }
   clk.mark();
   real_to_complex(s, n, n, Z, n, b2, ld);
-  tridiag_back(s, n, b0, ld, tau, ws_hetrd, b2, ld, n, ws_unmtr);
+  tridiag_back(s, n, b0, ld, tau, ws_hetrd, b2, ld, n, ws_unmtr, true);
   clk.mark();
   // lambda_from_squares (solvers.cpp:125)
   clamp_spectrum(s, n, d, 0, lam, flg, nonpos, counts, floor_p);
@@ -295,16 +300,21 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   // svd(C) (solvers.cpp:142): bidiagonalise, TGK divide & conquer, back-transform
   zgebrd_upper(s, n, b2, ld, d, e, tauq, taup, ws_gebrd);
   clk.mark();
+  // reflector blocks of Q and P (reflectors only) on the aux stream beside the D&C
+  fork(c);
+  prepare_reflectors(c->aux, 1, n, n, b2, ld, tauq, ws_unmbr);
+  prepare_reflectors(c->aux, 2, n, n - 1, b2, ld, taup, ws_unmbr2);
   tgk_build(s, n, d, e, td, te);
   dstedc(s, m2, td, te, X, ws_stedc, info + 2, n);  // only the positive half of the vectors
+  join(c);
   clk.mark();
   // ascending singular values = top n TGK eigenvalues; vectors u (b3), v (b4)
   BSE_CUDA(cudaMemcpyAsync(sasc, td + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   tgk_refine(s, n, d, e, sasc, te);  // relative accuracy of the small singular values
   tgk_extract(s, n, X, b3, ld, b4, ld);
   fork(c);
-  zunmbr_q(s, n, b2, ld, tauq, b3, ld, n, ws_unmbr);         // U = Q U_B
-  zunmbr_p(c->aux, n, b2, ld, taup, b4, ld, n, ws_unmbr2);   // V = P V_B (concurrently)
+  apply_prepared_reflectors(s, 1, n, n, b3, ld, n, ws_unmbr);             // U = Q U_B
+  apply_prepared_reflectors(c->aux, 2, n, n - 1, b4, ld, n, ws_unmbr2);   // V = P V_B
   join(c);
   clk.mark();
   {
