@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 from paper_2008_08825_b200 import configs  # noqa: E402
 
-OUT = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "full")
 
 
 def big_case(name, gen, seed, n, methods, note):

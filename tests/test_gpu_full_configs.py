@@ -20,7 +20,7 @@ from paper_2008_08825_b200 import configs
 from tests.helpers import EPS, norm_h
 
 pytestmark = pytest.mark.gpu
-GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full")
 
 
 def _load(name):
