@@ -93,6 +93,7 @@ int guarded(bse_ctx* c, bse_status* st, F&& fn) {
       g_timer = b;
     }
   } restore{prev, prev_timer};
+  const bseg::TridiagModeScope tridiag_mode;  // one reading of the reduction mode per call
   try {
     BSE_CUDA(cudaSetDevice(c->device));
     fn();
@@ -551,7 +552,9 @@ void run_batch(bse_ctx* c, const BatchIO& io, int64_t batch, int64_t* failed_ind
     }
     bse_ctx* lc = c->twin[l - 1];
     const int cap = g_panel_ctas;  // set above from `lanes`
-    extra.emplace_back([&, l, lc, cap] {
+    const int tmode = current_tridiag_mode();  // the caller's snapshot, for every lane
+    extra.emplace_back([&, l, lc, cap, tmode] {
+      const TridiagModeScope tridiag_mode(tmode);
       try {
         BSE_CUDA(cudaSetDevice(lc->device));
         g_launch_counter = &lc->launches;

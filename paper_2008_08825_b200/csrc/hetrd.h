@@ -43,6 +43,15 @@ void zunmtr_2stage(cudaStream_t s, int64_t n, const z_t* A, int64_t lda, const z
 // Two-stage reduction for this n in the current mode (batch lanes, or BSE_TWO_STAGE=1/0).
 bool use_two_stage(int64_t n);
 int set_tridiag_mode(int mode);  // bse_set_tridiagonal_reduction; returns the previous mode
+int current_tridiag_mode();      // this thread's snapshot if one is active, else the global
+// Holds one reading of the mode for this thread (outermost scope wins); mode < 0: read now.
+struct TridiagModeScope {
+  explicit TridiagModeScope(int mode = -1);
+  ~TridiagModeScope();
+  TridiagModeScope(const TridiagModeScope&) = delete;
+  TridiagModeScope& operator=(const TridiagModeScope&) = delete;
+  bool owner;
+};
 // The eigen-solvers' reduction pair, one- or two-stage per use_two_stage(n) (decided in the
 // calling thread; the same ws must reach tridiag_back).
 size_t tridiag_workspace_bytes(int64_t n);

@@ -635,9 +635,22 @@ std::atomic<int> g_tridiag_mode{[] {
 }()};
 }  // namespace
 
+// Per-call snapshot: a solve decides workspace size, reduction and back-transform from one
+// reading, so a concurrent bse_set_tridiagonal_reduction cannot split a solve's choices.
+thread_local int g_tridiag_snap = -1;
+
 int set_tridiag_mode(int mode) { return g_tridiag_mode.exchange(mode != 0 ? 1 : 0); }
 
-bool use_two_stage(int64_t n) { return n >= 4 * kB && g_tridiag_mode.load() != 0; }
+int current_tridiag_mode() { return g_tridiag_snap >= 0 ? g_tridiag_snap : g_tridiag_mode.load(); }
+
+TridiagModeScope::TridiagModeScope(int mode) : owner(g_tridiag_snap < 0) {
+  if (owner) g_tridiag_snap = mode >= 0 ? mode : g_tridiag_mode.load();
+}
+TridiagModeScope::~TridiagModeScope() {
+  if (owner) g_tridiag_snap = -1;
+}
+
+bool use_two_stage(int64_t n) { return n >= 4 * kB && current_tridiag_mode() != 0; }
 
 void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, double* e,
                    z_t* tau1, void* ws) {
