@@ -8,6 +8,8 @@
 // product_pair's definiteness certificates (core.cpp:87-100) keep their order and error
 // payloads; the certificate factor of A-B (CHOL) and both factors (CHOL+SVD) are reused
 // instead of recomputed (the reference runs potrf 3x / 4x).
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdlib>
 #include <cstring>
 
@@ -24,11 +26,30 @@ namespace {
 
 const z_t kOne = {1.0, 0.0}, kZero = {0.0, 0.0};
 
+// Phase boundaries: CUDA events on the solve's stream (bse_phase_times) and one NVTX range
+// per phase ("chol.reduce", ...; no-ops without a tool attached), so ncu can select a phase
+// with --nvtx --nvtx-include "chol.reduce/".
+constexpr const char* kPhaseNames[2][7] = {
+    {"chol.product_pair", "chol.certify", "chol.triple", "chol.reduce", "chol.tridiag",
+     "chol.backtransform", "chol.recover"},
+    {"chol-svd.product_pair", "chol-svd.certify", "chol-svd.triple", "chol-svd.reduce",
+     "chol-svd.tridiag", "chol-svd.backtransform", "chol-svd.recover"}};
+
 struct PhaseClock {
   bse_ctx* c;
+  const char* const* names;
   int k = 0;
-  explicit PhaseClock(bse_ctx* ctx) : c(ctx) { mark(); }
-  void mark() { BSE_CUDA(cudaEventRecord(c->ev[k++], c->stream)); }
+  bool open = false;
+  PhaseClock(bse_ctx* ctx, int method_row) : c(ctx), names(kPhaseNames[method_row]) { mark(); }
+  ~PhaseClock() {
+    if (open) nvtxRangePop();
+  }
+  void mark() {
+    BSE_CUDA(cudaEventRecord(c->ev[k++], c->stream));
+    if (open) nvtxRangePop();
+    open = k <= 7;
+    if (open) nvtxRangePushA(names[k - 1]);
+  }
   float between(int a, int b) {
     float ms = 0.f;
     BSE_CUDA(cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]));
@@ -165,7 +186,7 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
   const int64_t ld = n;
 
   z_t* ws_potrf2 = w.take<z_t>(64 * 64);
-  PhaseClock clk(c);
+  PhaseClock clk(c, 0);
   // product_pair: M1 -> b0, M2 -> b1 and the factor L = chol(M2) (reused, solvers.cpp:121).
   // The certificate of M1 comes from the spectrum of M below (certify_m1).
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
@@ -284,7 +305,7 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   z_t* ws_potrf = w.take<z_t>(64 * 64);
   const int64_t ld = n;
 
-  PhaseClock clk(c);
+  PhaseClock clk(c, 1);
   // product_pair + L1 = chol(M1), L2 = chol(M2) (solvers.cpp:138-140): b0 = L1, b1 = L2
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
   fork(c);
