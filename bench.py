@@ -234,6 +234,19 @@ def main():
     ms = ev0.elapsed_time(ev1)
     launches = ctx.kernel_launches() - launches0
     phase_hist = [ctx.phase_times()]  # lane 0's last solve, with per-kernel event timings
+    # untimed check of the last timed matrix on the device: residual / (||H||_F ||x||) and
+    # ||V^H Sigma V - I||_F (verify.cpp:70-93; the same bounds as the parity tests)
+    last = total - 1
+    res_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    bse.residual_device(n, d_in[last][0].data_ptr(), d_in[last][1].data_ptr(), n,
+                        d_lams[last].data_ptr(), d_vs[last % lanes].data_ptr(),
+                        res_dev.data_ptr(), ctx=ctx)
+    check = {"item_seed": seeds[last % pool],
+             "residual_max": (res_dev / torch.linalg.vector_norm(d_vs[last % lanes], dim=1)).max().item(),
+             "residual_bound": 100 * n * float(np.finfo(float).eps),
+             "sigma_dev": bse.sigma_orthogonality_error_device(2 * n, n, d_vs[last % lanes].data_ptr(),
+                                                               ctx=ctx)}
+    check["ok"] = bool(check["residual_max"] <= check["residual_bound"])
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -426,6 +439,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "check": check,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
