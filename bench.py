@@ -3,19 +3,28 @@
 
 Workload (config 5): a batch of 64 independent complex128 n=4096 BSE matrices (config-2
 generator, seeds 0..63), CHOL method, partitioned across ranks by seed (rank r solves seeds
-r, r+N, ...). One "step" = every rank solves one matrix of its shard (inputs resident in
-HBM, distinct seed per step); NCCL only gathers the per-matrix eigenvalues to all ranks.
+r, r+N, ...; one process per GPU). One "step" = every rank solves `--lanes` matrices of its
+shard concurrently (inputs resident in HBM); NCCL all-gathers the per-matrix eigenvalues
+inside the timed region. The optional eigenvector gather to rank 0 is timed separately.
 value = whole-job FP64 TFLOP/s under the reference flop model (160/3 n^3 real flops per
-complex CHOL solve, proj/src/bench.cpp:41-50 x4 for complex).
+complex CHOL solve, proj/src/bench.cpp:41-50 x4 for complex). A CHOL+SVD sub-block times the
+paper's second method in the same run (its own throughput, latency and roofline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 4096]
-                  [--method chol|chol-svd] [--no-cpu-baseline]
+                  [--method chol|chol-svd] [--lanes L] [--no-cpu-baseline] [--no-e2e]
+                  [--no-chol-svd] [--v-gather]
+
+--gpus N without torchrun re-executes this file under torch.distributed.run (N ranks on
+127.0.0.1). `--stub` swaps the GPU solver for a deterministic CPU stand-in on gloo so the
+rank spawn, seed partition, gathers and max-over-ranks timing run in the CPU test suite
+(tests/test_bench_dist.py); a stub line is never a measurement.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -28,18 +37,29 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 FLOP_COEFF = {"chol": 160.0 / 3.0, "chol-svd": 296.0 / 3.0}  # Table 1 x4 complex
+BATCH = 64  # config 5
 
 
 def flops(method: str, n: int) -> float:
     return FLOP_COEFF[method] * float(n) ** 3
 
 
-def load_peaks() -> dict:
+def load_json(*parts) -> dict:
     try:
-        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+        with open(os.path.join(HERE, *parts)) as f:
             return json.load(f)
     except Exception:
         return {}
+
+
+def fp64_peak() -> tuple:
+    """FP64 tensor (DMMA) peak: the committed probe output (tools/microbench/fp64_peak.cu run
+    on this pool's B200, profiles/fp64_peak.json); MEASURED_PEAKS.json carries no FP64 entry."""
+    p = load_json("profiles", "fp64_peak.json")
+    if p.get("fp64_dmma_tflops"):
+        return float(p["fp64_dmma_tflops"]), (
+            f"profiles/fp64_peak.json (DMMA m8n8k4 probe at {p.get('fp64_dmma_sm_mhz')} MHz)")
+    return 37.0, "fallback literal (profiles/fp64_peak.json missing)"
 
 
 class ClockSampler:
@@ -49,8 +69,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, enabled: bool = True):
         self.index = index
+        self.enabled = enabled
         self.samples = []
         self._stop = threading.Event()
         self._t = None
@@ -69,8 +90,9 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.enabled:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
@@ -94,27 +116,106 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def dist_init():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+# ------------------------------------------------------------------------ distributed plumbing
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N outside torchrun: re-execute this file as N ranks (one process per GPU)."""
+    env = dict(os.environ)
+    if not args.stub:
+        env.setdefault("NCCL_DEBUG", "INFO")  # the driver counts the ranks from NCCL's init lines
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+class Dist:
+    """One process per GPU: NCCL over NVLink/NVSwitch (gloo on CPU tensors for --stub)."""
+
+    def __init__(self, stub: bool):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
         import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return world, rank, local
+        if stub:
+            self.device = torch.device("cpu")
+        else:
+            torch.cuda.set_device(self.local)
+            self.device = torch.device("cuda", self.local)
+        if self.world > 1:
+            import torch.distributed as dist
+            if stub:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.device)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        """Max over ranks (every timed number is the slowest rank's)."""
+        if not self.dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_gather_lams(self, local):
+        """(k, n) eigenvalues of this rank's items -> (world, k, n) on every rank."""
+        import torch
+        out = torch.empty((self.world,) + tuple(local.shape), dtype=local.dtype,
+                          device=local.device)
+        if self.dist:
+            self.dist.all_gather_into_tensor(out, local.contiguous())
+        else:
+            out[0].copy_(local)
+        return out
+
+    def gather_v_to_rank0(self, vs, recv_buf):
+        """Eigenvectors of one step (this rank's `lanes` 2n x n blocks) to rank 0 by
+        point-to-point send/recv (NVLink under NCCL). Rank 0 receives into one reused buffer:
+        the transfer is what is timed, not a 32 GiB resident copy of config 5's V."""
+        got = 0
+        if not self.dist:
+            return got
+        if self.rank == 0:
+            for src in range(1, self.world):
+                for _ in vs:
+                    self.dist.recv(recv_buf, src=src)
+                    got += recv_buf.numel() * recv_buf.element_size()
+        else:
+            for v in vs:
+                self.dist.send(v, dst=0)
+        return got
+
+    def close(self):
+        if self.dist:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
 
 
-def seeds_for(rank: int, world: int, steps: int, offset: int = 0):
-    """Seed partition of the 64-matrix batch: rank r owns r, r+N, ...; step k -> k-th own seed."""
-    own = [s for s in range(64) if s % world == rank]
-    return [own[(offset + k) % len(own)] for k in range(steps)]
+def shard(rank: int, world: int):
+    """Seed partition of the 64-matrix batch: rank r owns r, r+N, ... (balanced for N | 64)."""
+    return [s for s in range(BATCH) if s % world == rank]
 
 
+# ------------------------------------------------------------------------ reference arm
 def run_reference(args):
-    """--impl reference: the reference's CPU path (LAPACK restatement, oracle/) on the host."""
-    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    """--impl reference: the reference's CPU path (LAPACK restatement, oracle/) on the host.
+    Inputs come from libbse_gen.so (host-only generator): the GPU library is never loaded."""
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
@@ -129,7 +230,7 @@ def run_reference(args):
         oracle.solve(method, a, b)
     times = []
     for k in range(args.steps):
-        a, b = configs.config5(k % 64, n=n)
+        a, b = configs.config5(k % BATCH, n=n)
         t0 = time.perf_counter()
         oracle.solve(method, a, b)
         times.append(time.perf_counter() - t0)
@@ -150,32 +251,97 @@ def run_reference(args):
                                    f"{oracle.blas_config().split()[1]})"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "s_per_solve": t / args.steps,
+        "s_per_solve_median": statistics.median(times),
+        "native_libs": sorted({os.path.basename(l.split()[-1]) for l in open("/proc/self/maps")
+                               if l.rstrip().endswith(".so") and "/bse" in l.split()[-1]}),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=4096)
-    ap.add_argument("--method", default="chol", choices=["chol", "chol-svd"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lanes", type=int, default=4, help="matrices in flight per GPU")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-
+# ------------------------------------------------------------------------ stub arm (CPU test)
+def run_stub(args, d: Dist):
+    """The same rank spawn / shard / all-gather / V-gather / max-over-ranks code with a CPU
+    stand-in solver (gloo). Eigenvalues of item seed s: s*1000 + arange(n)."""
     import torch
-    world, rank, local = dist_init()
-    torch.cuda.set_device(local)
+    n, lanes = args.n, max(1, args.lanes)
+    own = shard(d.rank, d.world)
+    total = (args.warmup + args.steps) * lanes
+    items = [own[i % len(own)] for i in range(total)]
+
+    def solve(seed):
+        lam = torch.arange(n, dtype=torch.float64) + 1000.0 * seed
+        v = torch.full((n, 2 * n), complex(seed, -seed), dtype=torch.complex128)
+        return lam, v
+
+    d.barrier()
+    t0 = time.perf_counter()
+    lams, vs = [], []
+    for s in items[args.warmup * lanes:]:
+        lam, v = solve(s)
+        lams.append(lam)
+        vs.append(v)
+    gathered = d.all_gather_lams(torch.stack(lams))
+    ms = d.max(1e3 * (time.perf_counter() - t0))
+    recv = torch.empty((n, 2 * n), dtype=torch.complex128)
+    vbytes = d.gather_v_to_rank0(vs[-lanes:], recv)
+    if d.rank == 0:
+        seeds_seen = sorted({int(round(float(g[0]) / 1000.0)) for g in gathered.reshape(-1, n)})
+        line = {"metric": "stub (CPU stand-in solver; not a measurement)", "value": None,
+                "unit": None, "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "stub": True,
+                "gathered_seeds": seeds_seen, "gathered_shape": list(gathered.shape),
+                "v_gather_bytes": vbytes, "v_last_rank1": complex(recv[0, 0]).real
+                if d.world > 1 else None,
+                "config": {"parallelism": f"dp{d.world} (seed partition, gloo stub)"}}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------ our arm
+def roofline_panel(ph, method, peaks, where, traffic):
+    ach = ph["panel_bytes"] / max(ph["panel_ms"], 1e-9) / 1e6  # GB/s
+    pk = peaks.get("hbm_gbs", 6540.8)
+    launches = max(ph["panel_launches"], 1)
+    rf = {"bound": "hbm",
+          "kernel": ("gebrd_panel_kernel" if method == "chol-svd" else "hetrd_panel_kernel")
+          + " (cooperative, TMA tile ring)",
+          "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
+          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else
+          "fallback (B200_PROFILING.md)",
+          "per_launch_ms": ph["panel_ms"] / launches,
+          "algorithmic_bytes_per_launch": ph["panel_bytes"] / launches,
+          "measured": where}
+    tr = traffic.get("gebrd" if method == "chol-svd" else "hetrd", {})
+    if "ratio" in tr:  # ncu dram bytes / algorithmic bytes of one captured launch
+        rf["traffic"] = tr["ratio"] * rf["algorithmic_bytes_per_launch"]
+        rf["traffic_source"] = tr.get("capture")
+    return rf
+
+
+def roofline_gemm(ph, peak, peak_src, where, traffic):
+    launches = max(ph["gemm_launches"], 1)
+    ach = ph["gemm_dmma_flops"] / max(ph["gemm_ms"], 1e-9) / 1e9  # TFLOP/s executed on DMMA
+    rf = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (DMMA.8x8x4; 3M complex)",
+          "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+          "peak_source": peak_src, "per_launch_ms": ph["gemm_ms"] / launches,
+          "complex_equivalent_tflops": ph["gemm_flops"] / max(ph["gemm_ms"], 1e-9) / 1e9,
+          "note": "achieved = real flops issued to the FP64 tensor pipe (3M: 6 per complex MAC) "
+                  "/ summed GEMM launch time", "measured": where}
+    tr = traffic.get("zgemm", {})
+    if "bytes_per_flop" in tr:
+        rf["traffic"] = tr["bytes_per_flop"] * ph["gemm_flops"] / launches
+        rf["traffic_unit"] = "bytes per launch (DRAM read + write)"
+        rf["traffic_source"] = tr.get("capture")
+    return rf
+
+
+def run_ours(args, d: Dist):
+    import torch
     import paper_2008_08825_b200 as bse
     from paper_2008_08825_b200 import configs
-    dev = torch.device("cuda", local)
+    dev = d.device
+    world, rank, local = d.world, d.rank, d.local
     n, method = args.n, args.method
     meth = bse.Method.Chol if method == "chol" else bse.Method.CholSvd
     ctx = bse.Context(local)
@@ -190,10 +356,10 @@ def main():
     total = (args.warmup + args.steps) * lanes
     # a pool of up to 8 distinct matrices per rank, item i -> pool[i % pool]: every input is
     # 512 MiB (> 126 MB L2), so cycling the pool needs no L2 flush between items
-    pool = min(total, 8)
-    seeds = seeds_for(rank, world, pool)
-    host_pool = []
-    dev_pool = []
+    own = shard(rank, world)
+    pool = min(total, 8, len(own))
+    seeds = own[:pool]
+    host_pool, dev_pool = [], []
     for sd in seeds:
         a, b = configs.config5(sd, n=n)
         ha = torch.from_numpy(a.T).pin_memory()  # same bytes, column-major complex128
@@ -203,37 +369,50 @@ def main():
     host = [host_pool[i % pool] for i in range(total)]
     d_in = [dev_pool[i % pool] for i in range(total)]
     torch.cuda.synchronize()
-    d_lams = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(total)]
+    d_lams = torch.empty((total, n), dtype=torch.float64, device=dev)
     d_vs = [torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)  # 2n x n col-major
             for _ in range(lanes)]  # item i writes lane i % lanes's buffer (sequential per lane)
-    lam_all = torch.empty((world, args.steps * lanes, n), dtype=torch.float64, device=dev)
 
-    def run_items(lo, hi):
-        bse.solve_batched_device(meth, n, [d_in[i][0].data_ptr() for i in range(lo, hi)],
+    def run_items(m, lo, hi):
+        bse.solve_batched_device(m, n, [d_in[i][0].data_ptr() for i in range(lo, hi)],
                                  [d_in[i][1].data_ptr() for i in range(lo, hi)],
                                  [d_lams[i].data_ptr() for i in range(lo, hi)],
                                  [d_vs[i % lanes].data_ptr() for i in range(lo, hi)], ctx=ctx)
 
-    run_items(0, args.warmup * lanes)
+    run_items(meth, 0, args.warmup * lanes)
     torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    d.barrier()
     launches0 = ctx.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        run_items(args.warmup * lanes, total)
-        if world > 1:  # every matrix's eigenvalues to every rank
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(lam_all, torch.stack(d_lams[args.warmup * lanes:]))
+        run_items(meth, args.warmup * lanes, total)
+        with torch.cuda.stream(stream):  # every matrix's eigenvalues to every rank (NCCL)
+            lam_all = d.all_gather_lams(d_lams[args.warmup * lanes:])
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    ms = d.max(ev0.elapsed_time(ev1))
     launches = ctx.kernel_launches() - launches0
-    phase_hist = [ctx.phase_times()]  # lane 0's last solve, with per-kernel event timings
+    ph = ctx.phase_times()  # lane 0's last solve, with per-kernel event timings
+    ms_per_step = ms / args.steps
+    value = world * lanes * flops(method, n) / (ms_per_step / 1e3) / 1e12
+
+    # optional eigenvector gather of one step to rank 0 (timed separately)
+    v_gather = None
+    if args.v_gather and world > 1:
+        recv = torch.empty((n, 2 * n), dtype=torch.complex128, device=dev) if rank == 0 else None
+        d.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        got = d.gather_v_to_rank0(d_vs, recv)
+        torch.cuda.synchronize()
+        gms = d.max(1e3 * (time.perf_counter() - t0))
+        v_gather = {"ms": gms, "bytes_to_rank0": got, "GB_per_s": got / gms / 1e6 if gms else None,
+                    "what": f"one step's V ({lanes} x 512 MiB per rank) to rank 0 by NCCL "
+                            "send/recv, after the timed region"}
+
     # untimed check of the last timed matrix on the device: residual / (||H||_F ||x||) and
     # ||V^H Sigma V - I||_F (verify.cpp:70-93; the same bounds as the parity tests)
     last = total - 1
@@ -245,26 +424,52 @@ def main():
              "residual_max": (res_dev / torch.linalg.vector_norm(d_vs[last % lanes], dim=1)).max().item(),
              "residual_bound": 100 * n * float(np.finfo(float).eps),
              "sigma_dev": bse.sigma_orthogonality_error_device(2 * n, n, d_vs[last % lanes].data_ptr(),
-                                                               ctx=ctx)}
-    check["ok"] = bool(check["residual_max"] <= check["residual_bound"])
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
-    value = world * lanes * flops(method, n) / (ms_per_step / 1e3) / 1e12
-    # latency of one solve alone (whole GPU, no concurrent lane), for reference
-    torch.cuda.synchronize()
-    l0 = torch.cuda.Event(enable_timing=True)
-    l1 = torch.cuda.Event(enable_timing=True)
-    l0.record(stream)
-    for i in range(2):
-        bse.solve_device(meth, n, d_in[i][0].data_ptr(), d_in[i][1].data_ptr(),
-                         d_lams[i].data_ptr(), d_vs[0].data_ptr(), ctx=ctx)
-    l1.record(stream)
-    torch.cuda.synchronize()
-    single_ms = l0.elapsed_time(l1) / 2
-    ph_single = ctx.phase_times()  # per-kernel event timings of a solve that owns the GPU
+                                                               ctx=ctx),
+             "gathered_lams_finite": bool(torch.isfinite(lam_all).all().item())}
+    check["ok"] = bool(check["residual_max"] <= check["residual_bound"] and check["sigma_dev"] <= 1e-8)
+
+    def single_latency(m, reps=2):
+        """one solve alone on the whole GPU (no concurrent lane)"""
+        torch.cuda.synchronize()
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        for i in range(reps):
+            bse.solve_device(m, n, d_in[i][0].data_ptr(), d_in[i][1].data_ptr(),
+                             d_lams[i].data_ptr(), d_vs[0].data_ptr(), ctx=ctx)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        return l0.elapsed_time(l1) / reps, ctx.phase_times()
+
+    single_ms, ph_single = single_latency(meth)
+
+    # ---- CHOL+SVD in the same run (the paper's second method; reference bench.cpp:155, 190-204)
+    svd_block = None
+    if method == "chol" and not args.no_chol_svd:
+        ks = min(args.steps, 3)
+        run_items(bse.Method.CholSvd, 0, lanes)  # warm-up: workspaces of the SVD route
+        torch.cuda.synchronize()
+        d.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_items(bse.Method.CholSvd, lanes, lanes + ks * lanes)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sms = d.max(e0.elapsed_time(e1))
+        ph_svd_lane = ctx.phase_times()
+        svd_single_ms, ph_svd = single_latency(bse.Method.CholSvd)
+        svd_block = {
+            "metric": f"BSE eigensolve FP64 TFLOP/s (Table-1 flop model), n={n} c128, chol-svd",
+            "value": world * lanes * flops("chol-svd", n) / (sms / ks / 1e3) / 1e12,
+            "unit": "TFLOP/s", "steps": ks, "matrices_per_step_per_gpu": lanes,
+            "ms_per_step": sms / ks, "s_per_solve": sms / ks / lanes / 1e3,
+            "single_solve_latency_ms": svd_single_ms,
+            "phase_ms": {k: round(v, 3) for k, v in ph_svd.items()
+                         if k in ("product_pair", "triple", "reduce", "tridiag", "backtransform",
+                                  "recover", "total")},
+            "lane_panel": {"ms": ph_svd_lane["panel_ms"], "launches": ph_svd_lane["panel_launches"]},
+            "ph_single": ph_svd}
 
     # ---- end to end through the host-pointer C-ABI: every step's inputs go H2D from pinned
     # host memory and its (lambda, V) come back D2H inside the timed region. Headline: the
@@ -310,8 +515,7 @@ def main():
                 raise RuntimeError(st.message.decode())
 
         def timed(fn):
-            if world > 1:
-                dist.barrier()
+            d.barrier()
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -319,12 +523,7 @@ def main():
             fn()
             e1.record(stream)
             torch.cuda.synchronize()
-            ems = e0.elapsed_time(e1)
-            if world > 1:
-                t = torch.tensor([ems], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ems = float(t.item())
-            return ems
+            return d.max(e0.elapsed_time(e1))
 
         batched(host[: args.warmup * lanes])  # untimed: staging buffers, lane contexts
         ems = timed(lambda: batched(host[args.warmup * lanes: total]))
@@ -343,72 +542,48 @@ def main():
                                "path": "one bse_solve per matrix, one matrix at a time (pinned; "
                                        "V streamed back in chunks)"}}
 
-    # ---- roofline of the dominant kernel class from the live event timings
-    peaks = load_peaks()
-    fp64_peak = 37.0  # DMMA m8n8k4 issue-rate probe on this pool (tools/microbench/fp64_peak.cu)
+    # ---- rooflines: the reduction panel against HBM and the DMMA GEMMs against the FP64
+    # tensor peak, both from the live event timings (lane 0 in the timed region, and a solve
+    # that owns the GPU); `roofline` is the class with the larger share of lane 0's time
+    peaks = load_json("MEASURED_PEAKS.json")
+    traffic = load_json("profiles", "traffic.json")
+    peak64, peak64_src = fp64_peak()
+    lane_where = (f"timed region, lane 0 of {lanes}: each kernel runs beside the other lanes' "
+                  "work (1/lanes of the SMs for the panels)")
+    whole_where = "single-solve pass: the kernel owns the GPU"
+    rf_panel = roofline_panel(ph, method, peaks, lane_where, traffic)
+    rf_gemm = roofline_gemm(ph, peak64, peak64_src, lane_where, traffic)
+    rf_panel_w = roofline_panel(ph_single, method, peaks, whole_where, traffic)
+    rf_gemm_w = roofline_gemm(ph_single, peak64, peak64_src, whole_where, traffic)
+    roofline = rf_panel if ph["panel_ms"] >= ph["gemm_ms"] else rf_gemm
 
-    def roofline_of(ph, where):
-        panel = {"ms": ph["panel_ms"], "launches": ph["panel_launches"], "bytes": ph["panel_bytes"]}
-        gemm = {"ms": ph["gemm_ms"], "launches": ph["gemm_launches"], "flops": ph["gemm_flops"]}
-        if panel["ms"] >= gemm["ms"]:
-            ach = panel["bytes"] / (panel["ms"] / 1e3) / 1e9
-            pk = peaks.get("hbm_gbs", 6650.0)
-            rf = {"bound": "hbm",
-                  "kernel": ("gebrd_panel_kernel" if method == "chol-svd" else "hetrd_panel_kernel")
-                  + " (cooperative, TMA tile ring)",
-                  "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
-                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                  "per_launch_ms": panel["ms"] / max(panel["launches"], 1),
-                  "algorithmic_bytes_per_launch": panel["bytes"] / max(panel["launches"], 1)}
-        else:
-            ach = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12
-            rf = {"bound": "tensor", "kernel": "zgemm_dmma_kernel (DMMA.8x8x4, 3M)",
-                  "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                  "traffic": None,
-                  "peak_source": "measured FP64 DMMA probe (MEASURED_PEAKS.json has no FP64)",
-                  "per_launch_ms": gemm["ms"] / max(gemm["launches"], 1)}
-        rf["measured"] = where
-        try:
-            with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
-                tr = json.load(f).get(rf["bound"], {})
-            if rf["bound"] == "hbm" and "ratio" in tr:
-                # ncu dram bytes / algorithmic bytes of one captured launch, applied per launch
-                trk = tr.get("gebrd", tr) if method == "chol-svd" else tr
-                rf["traffic"] = trk["ratio"] * rf["algorithmic_bytes_per_launch"]
-                rf["traffic_source"] = trk.get("capture")
-            if rf["bound"] == "tensor" and "bytes_per_flop" in tr:
-                rf["traffic"] = tr["bytes_per_flop"] * gemm["flops"] / max(gemm["launches"], 1)
-                rf["traffic_unit"] = "bytes per launch (DRAM read + write)"
-                rf["traffic_source"] = tr.get("capture")
-        except Exception:
-            pass
-        return rf, panel, gemm
-
-    ph = phase_hist[-1]
-    roofline, panel, gemm = roofline_of(
-        ph, f"timed region, lane 0 of {lanes}: each panel kernel runs on 1/{lanes} of the SMs "
-            f"beside the other lanes' work")
-    roofline_whole, _, _ = roofline_of(ph_single, "single-solve pass: the kernel owns the GPU")
+    # FP64 tensor-pipe utilisation over the whole timed region (executed DMMA flops of every
+    # solve / (time x GPUs x peak)); the Table-1 model figure is reported beside it
+    dmma_per_solve = ph["gemm_dmma_flops"]
+    fp64_exec_frac = dmma_per_solve * lanes * args.steps / (ms / 1e3) / 1e12 / peak64
+    # Cholesky phase (product_pair: A+-B and potrf of A-B, 4/3 n^3 complex = 16/3 n^3 real
+    # model flops) of a solve that owns the GPU
+    chol_tflops = (16.0 / 3.0) * n ** 3 / (ph_single["product_pair"] / 1e3) / 1e12
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         cores = os.cpu_count() or 1
         oracle.set_threads(cores)
-        # bounded sample (~10-30 s of CPU work): one full solve for CHOL; for CHOL+SVD the
-        # oracle's zgesvd('A','A') needs ~10-40 min at n = 4096, so the sample is n = 1024
-        n_cpu = n if method == "chol" else min(n, 1024)
-        a, b = configs.config5(seeds[args.warmup % pool], n=n_cpu)
+        # bounded sample (~10-30 s of CPU work): one full CHOL solve at the bench size
+        a, b = configs.config5(seeds[args.warmup % pool], n=n)
         t0 = time.perf_counter()
-        oracle.solve(method, a, b)
+        oracle.solve("chol", a, b)
         tc = time.perf_counter() - t0
-        cpu = {"value": flops(method, n_cpu) / tc / 1e12, "unit": "TFLOP/s", "cores": cores,
-               "kind": "port", "s_per_solve": tc, "n": n_cpu,
-               "sample": f"one {method} solve of config-5 seed {seeds[args.warmup % pool]} "
-                         f"(n={n_cpu}{'' if n_cpu == n else ', reduced from ' + str(n)}) with "
-                         f"the oracle/ LAPACK restatement on {cores} host threads"}
+        cpu = {"value": flops("chol", n) / tc / 1e12, "unit": "TFLOP/s", "cores": cores,
+               "kind": "port", "s_per_solve": tc, "n": n,
+               "sample": f"one chol solve of config-5 seed {seeds[args.warmup % pool]} (n={n}) "
+                         f"with the oracle/ LAPACK restatement on {cores} host threads"}
 
+    line = None
     if rank == 0:
+        phase_keys = ("product_pair", "triple", "reduce", "tridiag", "backtransform", "recover",
+                      "total")
         line = {
             "metric": f"BSE eigensolve FP64 TFLOP/s (Table-1 flop model), n={n} c128, {method}",
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -418,35 +593,79 @@ def main():
                                    f"(config-2 generator, seeds 0..63), {method}; each step every "
                                    f"GPU solves {lanes} matrices of its seed shard concurrently "
                                    "(bse_solve_batched_device, one lane per matrix)",
-                       "n": n, "method": method, "batch": 64, "matrices_per_step_per_gpu": lanes,
+                       "n": n, "method": method, "batch": BATCH, "matrices_per_step_per_gpu": lanes,
                        "l2": "inputs 512 MiB per solve (> 126 MB L2); a pool of up to 8 "
                              "distinct matrices per rank, cycled",
-                       "parallelism": f"dp{world} (seed partition, NCCL gathers eigenvalues)"},
+                       "parallelism": f"dp{world} (seed partition, NCCL all-gathers eigenvalues "
+                                      "inside the timed region)"},
             "s_per_solve": ms_per_step / 1e3 / lanes,
             "single_solve_latency_ms": single_ms,
-            "batch64_s": ms_per_step / 1e3 / lanes * 64 / world,
-            "fp64_frac_of_peak": value / (world * fp64_peak),
-            "phase_ms": {k: round(v, 3) for k, v in ph_single.items()
-                         if k in ("product_pair", "triple", "reduce", "tridiag", "backtransform",
-                                  "recover", "total")},  # one solve alone on the whole GPU
-            "phase_ms_batch_lane0": {k: round(v, 3) for k, v in ph.items()
-                                     if k in ("product_pair", "triple", "reduce", "tridiag",
-                                              "backtransform", "recover", "total")},
-            "kernels": {"panel": panel, "gemm": gemm,
-                        "gemm_tflops": gemm["flops"] / max(gemm["ms"], 1e-9) / 1e9},
+            "batch64_s": ms_per_step / 1e3 / lanes * BATCH / world,
+            "model_tflops_over_dmma_peak": value / (world * peak64),
+            "fp64_exec_frac": fp64_exec_frac,
+            "fp64_exec_note": "real flops issued to the DMMA pipe by the GEMMs per solve x solves "
+                              "/ (timed region x GPUs x FP64 tensor peak)",
+            "fp64_peak_tflops": peak64, "fp64_peak_source": peak64_src,
+            "cholesky_phase": {"ms": ph_single["product_pair"], "model_tflops": chol_tflops,
+                               "frac_of_dmma_peak": chol_tflops / peak64,
+                               "what": "A+-B and potrf(A-B) of one solve owning the GPU; "
+                                       "model flops 16/3 n^3 (complex potrf x4)"},
+            "phase_ms": {k: round(v, 3) for k, v in ph_single.items() if k in phase_keys},
+            "phase_ms_batch_lane0": {k: round(v, 3) for k, v in ph.items() if k in phase_keys},
+            "kernels": {"panel": {"ms": ph["panel_ms"], "launches": ph["panel_launches"],
+                                  "bytes": ph["panel_bytes"]},
+                        "gemm": {"ms": ph["gemm_ms"], "launches": ph["gemm_launches"],
+                                 "complex_equiv_flops": ph["gemm_flops"],
+                                 "dmma_flops": ph["gemm_dmma_flops"]}},
             "roofline": roofline,
-            "roofline_whole_gpu": roofline_whole,
+            "roofline_panel": rf_panel, "roofline_gemm": rf_gemm,
+            "roofline_whole_gpu": {"panel": rf_panel_w, "gemm": rf_gemm_w},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "v_gather": v_gather,
             "gpu_launches": int(launches),
             "check": check,
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        if svd_block:
+            psvd = svd_block.pop("ph_single")
+            svd_block["roofline_whole_gpu"] = {
+                "panel": roofline_panel(psvd, "chol-svd", peaks, whole_where, traffic),
+                "gemm": roofline_gemm(psvd, peak64, peak64_src, whole_where, traffic)}
+            line["chol_svd"] = svd_block
     ctx.close()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--method", default="chol", choices=["chol", "chol-svd"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-chol-svd", action="store_true", help="skip the CHOL+SVD sub-block")
+    ap.add_argument("--v-gather", action="store_true",
+                    help="N>1: also time one step's eigenvector gather to rank 0")
+    ap.add_argument("--lanes", type=int, default=4, help="matrices in flight per GPU")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU test hook
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    d = Dist(args.stub)
+    if args.stub:
+        rc = run_stub(args, d)
+        d.close()
+        return rc
+    line = run_ours(args, d)
+    d.close()
+    if line is not None:  # last: after NCCL's teardown messages
+        print(json.dumps(line), flush=True)
     return 0
 
 

@@ -86,7 +86,10 @@ typedef struct bse_phase_times {
   double panel_bytes;   /* algorithmic HBM bytes those launches must stream               */
   double gemm_ms;       /* sum over DMMA GEMM launches of the solve                        */
   double gemm_launches;
-  double gemm_flops;    /* executed real flops of those GEMM launches                      */
+  double gemm_flops;    /* complex-equivalent real flops of those GEMM launches (8 per      */
+                        /* complex MAC executed, triangular skipping counted)               */
+  double gemm_dmma_flops; /* real flops the FP64 tensor pipe executed for them (the 3M      */
+                        /* kernels issue 3 real DMMA MACs per complex MAC: 6 flops)         */
 } bse_phase_times;
 
 /* ---------------------------------------------------------------- context */
@@ -174,6 +177,18 @@ int bse_assemble_eigenvectors(bse_ctx* ctx, int64_t n, int64_t k,
                               const double* v1, int64_t ldv1, const double* v2, int64_t ldv2,
                               const double* lambda1, const double* lambda2,
                               double* v, int64_t ldv, bse_status* st);
+
+/* The eigenvector recovery tail of bse::solve_chol / solve_sqrt (solvers.cpp:125, 130-133):
+ * lambda_from_squares(d) (solvers.cpp:25-45: lambda = sqrt(d), clamped at eps*sqrt(d_max)
+ * and flagged), assemble_eigenvectors with factors (lambda^2, 1) (core.cpp:102-127), then
+ * rebuild_nonpositive_columns (solvers.cpp:53-65) for every d_j <= 0. v1, v2 n x k; d k
+ * (ascending); lambda k; v 2n x k; near_singular capacity k. BSE_ERR_CONVERGENCE_FAILURE
+ * when d_max <= 0. This is the device code the CHOL solve runs after its eigensolve,
+ * exposed so the breakdown rebuild can be checked column by column against the oracle. */
+int bse_assemble_from_squares(bse_ctx* ctx, int64_t n, int64_t k,
+                              const double* v1, int64_t ldv1, const double* v2, int64_t ldv2,
+                              const double* d, double* lambda, double* v, int64_t ldv,
+                              int64_t* near_singular, int64_t* n_near_singular, bse_status* st);
 
 /* ---------------------------------------------------------------- dense backend (backend.cpp) */
 /* cholesky_lower (backend.cpp:47-62): zpotrf 'L'; strict upper of l zeroed.             */

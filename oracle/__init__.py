@@ -174,3 +174,20 @@ def assemble_eigenvectors(v1, v2, l1, l2):
                                               _p(v2), _p(l1), _p(l2), _p(v),
                                               ctypes.byref(st)), st)
     return v
+
+
+def assemble_from_squares(v1, v2, d):
+    """solvers.cpp:125, 130-133: (lambda, V, near_singular) from the squared spectrum d and
+    the factors V1, V2, including the breakdown rebuild (solvers.cpp:53-65)."""
+    v1, v2 = _c(v1), _c(v2)
+    n, k = v1.shape
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    lam = np.zeros(k)
+    v = np.zeros((2 * n, k), dtype=np.complex128, order="F")
+    flags = np.zeros(k, dtype=np.int64)
+    nf = ctypes.c_int64(0)
+    st = Status()
+    _check(lib().oracle_assemble_from_squares(ctypes.c_int64(n), ctypes.c_int64(k), _p(v1),
+                                              _p(v2), _p(d), _p(lam), _p(v), _p(flags),
+                                              ctypes.byref(nf), ctypes.byref(st)), st)
+    return lam, v, flags[: nf.value].copy()

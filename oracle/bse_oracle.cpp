@@ -613,4 +613,29 @@ int oracle_assemble_eigenvectors(int64_t n, int64_t k, const double* v1, const d
   }
 }
 
+// solvers.cpp:125, 130-133 (the recovery tail of solve_chol / solve_sqrt): lambda_from_squares,
+// assemble_eigenvectors with (lambda^2, 1), rebuild_nonpositive_columns.
+int oracle_assemble_from_squares(int64_t n, int64_t k, const double* v1, const double* v2,
+                                 const double* d, double* lambda, double* v,
+                                 int64_t* near_singular, int64_t* n_near_singular,
+                                 bse_status* st) {
+  try {
+    const std::vector<double> w(d, d + k);
+    const Clamped cs = lambda_from_squares(w);
+    std::vector<double> l1(static_cast<size_t>(k)), ones(static_cast<size_t>(k), 1.0);
+    for (int64_t j = 0; j < k; ++j)
+      l1[static_cast<size_t>(j)] = cs.lambda[static_cast<size_t>(j)] * cs.lambda[static_cast<size_t>(j)];
+    const Mat m1 = load(n, k, v1, n), m2 = load(n, k, v2, n);
+    Mat vv = assemble_eigenvectors(m1, m2, l1, ones);
+    rebuild_nonpositive_columns(vv, m1, m2, w, cs);
+    std::memcpy(lambda, cs.lambda.data(), sizeof(double) * cs.lambda.size());
+    for (size_t i = 0; i < cs.flagged.size(); ++i) near_singular[i] = cs.flagged[i];
+    *n_near_singular = static_cast<int64_t>(cs.flagged.size());
+    store(vv, v, 2 * n);
+    return ok(st);
+  } catch (const Err& e) {
+    return fail(e, st);
+  }
+}
+
 }  // extern "C"

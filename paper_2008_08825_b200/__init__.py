@@ -365,6 +365,30 @@ def assemble_eigenvectors(f: HalfSpectralFactors, ctx: Optional[Context] = None)
     return v
 
 
+def assemble_from_squares(v1: np.ndarray, v2: np.ndarray, d: np.ndarray,
+                          ctx: Optional[Context] = None):
+    """The recovery tail of solve_chol / solve_sqrt on the device (solvers.cpp:125, 130-133):
+    lambda_from_squares(d), assemble_eigenvectors with (lambda^2, 1) and the breakdown rebuild
+    of every column with d_j <= 0 (solvers.cpp:53-65). Returns (lambda, V, near_singular)."""
+    ctx = ctx or default_context()
+    v1, v2 = _cm(v1), _cm(v2)
+    if v1.ndim != 2 or v2.shape != v1.shape:
+        raise DimensionMismatch("factor shapes do not conform")
+    n, k = v1.shape
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    if d.shape != (k,):
+        raise DimensionMismatch("factor shapes do not conform")
+    lam = np.zeros(k)
+    v = np.zeros((2 * n, k), dtype=np.complex128, order="F")
+    ns = np.zeros(k, dtype=np.int64)
+    nn = ctypes.c_int64(0)
+    st = Status()
+    _check(_lib.lib().bse_assemble_from_squares(ctx.handle, n, k, _p(v1), n, _p(v2), n, _p(d),
+                                                _p(lam), _p(v), 2 * n, _p(ns), ctypes.byref(nn),
+                                                ctypes.byref(st)), st)
+    return lam, v, ns[: nn.value].copy()
+
+
 # --------------------------------------------------------------------------- solvers (solvers.cpp)
 def _solve(method: Method, h: BseMatrixI, ctx: Optional[Context]) -> SpectralResult:
     ctx = ctx or default_context()

@@ -32,7 +32,7 @@ class PhaseTimes(ctypes.Structure):
     _fields_ = [(k, ctypes.c_double) for k in (
         "product_pair", "cholesky", "triple", "reduce", "tridiag", "backtransform", "recover",
         "total", "panel_ms", "panel_launches", "panel_bytes", "gemm_ms", "gemm_launches",
-        "gemm_flops")]
+        "gemm_flops", "gemm_dmma_flops")]
 
 
 # (name, restype, argtypes) for every symbol include/bse_gpu.h declares.
@@ -59,6 +59,9 @@ SYMBOLS = {
                                  ctypes.POINTER(Status)]),
     "bse_assemble_eigenvectors": (c_int, [c_dp, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp,
                                           c_dp, c_dp, c_i64, ctypes.POINTER(Status)]),
+    "bse_assemble_from_squares": (c_int, [c_dp, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp,
+                                          c_dp, c_dp, c_i64, c_dp, c_dp,
+                                          ctypes.POINTER(Status)]),
     "bse_cholesky_lower": (c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_i64,
                                    ctypes.POINTER(Status)]),
     "bse_matmul": (c_int, [c_dp, c_i64, c_i64, c_dp, c_i64, c_int, c_int, c_i64, c_i64, c_dp,

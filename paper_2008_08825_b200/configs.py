@@ -1,22 +1,47 @@
 """Seeded synthetic inputs: BASELINE.json configs 1-5 and the reference's test families.
 
-Input synthesis only (host numpy + the library's counter-based generator); not part of the
-timed hot path. The reference's public benchmark has no dataset: these generators stand in
+Input synthesis only (host numpy + the counter-based generator in ``libbse_gen.so``, a
+host-only library built from csrc/gen.cpp without any CUDA code, so loading the inputs never
+maps the GPU library ``libbse_b200.so``); not part of the timed hot path. The reference's public benchmark has no dataset: these generators stand in
 for it with its stated shapes, sizes and value distributions (BASELINE.json "configs").
 """
 from __future__ import annotations
 
 import ctypes
+import os
+import threading
 
 import numpy as np
 
-from . import _lib
+_GEN_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbse_gen.so")
+_gen = None
+_gen_lock = threading.Lock()
+
+
+def gen_lib():
+    """The host generator library (same bse_gen_* entry points as include/bse_gpu.h)."""
+    global _gen
+    with _gen_lock:
+        if _gen is None:
+            if not os.path.exists(_GEN_PATH):
+                raise RuntimeError(f"{_GEN_PATH} is missing: build it with `make -C "
+                                   f"{os.path.dirname(_GEN_PATH)}`")
+            L = ctypes.CDLL(_GEN_PATH)
+            c_u64, c_i64, c_dp, c_d = ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
+            L.bse_gen_dominant.argtypes = [c_i64, c_u64, ctypes.c_int, c_d, c_d, c_d, c_dp, c_dp]
+            for name in ("bse_gen_gaussian_stream", "bse_gen_normal", "bse_gen_uniform"):
+                getattr(L, name).argtypes = [c_u64, c_u64, c_i64, c_dp]
+            for name in ("bse_gen_dominant", "bse_gen_gaussian_stream", "bse_gen_normal",
+                         "bse_gen_uniform"):
+                getattr(L, name).restype = ctypes.c_int
+            _gen = L
+    return _gen
 
 
 def _gen_dominant(n: int, seed: int, is_complex: bool, scale: float, dlo: float, dhi: float):
     a = np.zeros((n, n), dtype=np.complex128, order="F")
     b = np.zeros((n, n), dtype=np.complex128, order="F")
-    rc = _lib.lib().bse_gen_dominant(n, seed, 1 if is_complex else 0, scale, dlo, dhi,
+    rc = gen_lib().bse_gen_dominant(n, seed, 1 if is_complex else 0, scale, dlo, dhi,
                                      a.ctypes.data_as(ctypes.c_void_p),
                                      b.ctypes.data_as(ctypes.c_void_p))
     if rc != 0:
@@ -26,13 +51,13 @@ def _gen_dominant(n: int, seed: int, is_complex: bool, scale: float, dlo: float,
 
 def normal(seed: int, stream: int, count: int) -> np.ndarray:
     out = np.zeros(count)
-    _lib.lib().bse_gen_normal(seed, stream, count, out.ctypes.data_as(ctypes.c_void_p))
+    gen_lib().bse_gen_normal(seed, stream, count, out.ctypes.data_as(ctypes.c_void_p))
     return out
 
 
 def uniform(seed: int, stream: int, count: int) -> np.ndarray:
     out = np.zeros(count)
-    _lib.lib().bse_gen_uniform(seed, stream, count, out.ctypes.data_as(ctypes.c_void_p))
+    gen_lib().bse_gen_uniform(seed, stream, count, out.ctypes.data_as(ctypes.c_void_p))
     return out
 
 
@@ -86,7 +111,7 @@ def config3(seed: int = 0, n: int = 4096):
 def gaussian_stream(seed: int, stream: int, count: int) -> np.ndarray:
     """proj/src/gen.cpp:19-38 GaussianStream::next_complex() x count (bit-exact port)."""
     out = np.zeros(2 * count)
-    _lib.lib().bse_gen_gaussian_stream(seed, stream, count, out.ctypes.data_as(ctypes.c_void_p))
+    gen_lib().bse_gen_gaussian_stream(seed, stream, count, out.ctypes.data_as(ctypes.c_void_p))
     return out[0::2] + 1j * out[1::2]
 
 

@@ -149,8 +149,13 @@ void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_
            const z_t* A, int64_t lda, const z_t* B, int64_t ldb, z_t beta, z_t* C, int64_t ldc,
            int a_shape, int b_shape, int c_lower, z_t* ws, int64_t ws_elems) {
   if (m <= 0 || n <= 0) return;
-  const int slot =
-      g_timer ? timer_begin(s, 0, zgemm_exec_flops(m, n, k, a_shape, b_shape, c_lower)) : -1;
+  // the 3M kernel runs 64x32 tiles, 3 resident CTAs per SM; the 4M kernels 64x64, 2 per SM
+  const bool m3 = g3m_mode() == 3 || (g3m_mode() && k > 128);
+  int slot = -1;
+  if (g_timer) {  // complex-equivalent flops, and the DMMA flops: 3 real MACs per complex MAC in 3M
+    const double f = zgemm_exec_flops(m, n, k, a_shape, b_shape, c_lower);
+    slot = timer_begin(s, 0, f, m3 ? 0.75 * f : f);
+  }
   struct End {
     cudaStream_t s;
     int slot;
@@ -162,8 +167,6 @@ void zgemm(cudaStream_t s, int opa, int opb, int64_t m, int64_t n, int64_t k, z_
   p.alpha = alpha; p.beta = beta;
   p.a_shape = a_shape; p.b_shape = b_shape; p.c_lower = c_lower;
   p.ksplit = 1;
-  // the 3M kernel runs 64x32 tiles, 3 resident CTAs per SM; the 4M kernels 64x64, 2 per SM
-  const bool m3 = g3m_mode() == 3 || (g3m_mode() && k > 128);
   const int64_t tiles_m = ceil_div(m, kBM), tiles_n = ceil_div(n, m3 ? 32 : kBN);
   int ksplit = 1;
   // Under-filled grid with a long K: split K across CTAs (deterministic two-pass reduce).

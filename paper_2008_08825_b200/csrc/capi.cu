@@ -113,7 +113,7 @@ void collect_timer(bse_ctx* c) {
   if (!c->timing) return;
   BSE_CUDA(cudaStreamSynchronize(c->stream));
   bse_phase_times& t = c->last;
-  t.panel_ms = t.gemm_ms = t.panel_bytes = t.gemm_flops = 0.0;
+  t.panel_ms = t.gemm_ms = t.panel_bytes = t.gemm_flops = t.gemm_dmma_flops = 0.0;
   t.panel_launches = t.gemm_launches = 0.0;
   for (int i = 0; i < c->timer.used / 2; ++i) {
     float ms = 0.f;
@@ -121,6 +121,7 @@ void collect_timer(bse_ctx* c) {
     if (c->timer.kind[i] == 0) {
       t.gemm_ms += ms;
       t.gemm_flops += c->timer.work[i];
+      t.gemm_dmma_flops += c->timer.work2[i];
       t.gemm_launches += 1;
     } else {
       t.panel_ms += ms;
@@ -693,6 +694,51 @@ int bse_assemble_eigenvectors(bse_ctx* c, int64_t n, int64_t k, const double* v1
     BSE_CUDA(cudaMemcpyAsync(l1, lambda1, sizeof(double) * size_t(k), cudaMemcpyHostToDevice, c->stream));
     BSE_CUDA(cudaMemcpyAsync(l2, lambda2, sizeof(double) * size_t(k), cudaMemcpyHostToDevice, c->stream));
     assemble(c->stream, n, k, d1, n, d2, n, l1, l2, 0, nullptr, l1, dV, 2 * n);
+    d2h(c, v, ldv, dV, 2 * n, 2 * n, k);
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bse_assemble_from_squares(bse_ctx* c, int64_t n, int64_t k, const double* v1,
+                              int64_t ldv1, const double* v2, int64_t ldv2, const double* d,
+                              double* lambda, double* v, int64_t ldv, int64_t* near_singular,
+                              int64_t* n_near_singular, bse_status* st) {
+  return guarded(c, st, [&] {
+    if (n < 1 || k < 1 || ldv1 < n || ldv2 < n || ldv < 2 * n)
+      throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "factor shapes do not conform"};
+    const size_t nk = size_t(n) * size_t(k);
+    DevBuf buf(nk * 4 * sizeof(z_t) + 3 * size_t(k) * sizeof(double) +
+                   2 * size_t(k) * sizeof(int64_t) + 8 * sizeof(int64_t) + 64,
+               c->stream);
+    z_t* d1 = buf.as<z_t>();
+    z_t* d2 = d1 + nk;
+    z_t* dV = d2 + nk;
+    double* dd = reinterpret_cast<double*>(dV + 2 * nk);
+    double* lam = dd + k;
+    double* l1 = lam + k;
+    int64_t* flg = reinterpret_cast<int64_t*>(l1 + k);
+    int64_t* nonpos = flg + k;
+    int64_t* counts = nonpos + k;
+    double* floor_p = reinterpret_cast<double*>(counts + 4);
+    h2d(c, d1, n, v1, ldv1, n, k);
+    h2d(c, d2, n, v2, ldv2, n, k);
+    BSE_CUDA(cudaMemcpyAsync(dd, d, sizeof(double) * size_t(k), cudaMemcpyHostToDevice, c->stream));
+    // the same launches as the tail of solve_chol_dev (solvers.cu)
+    clamp_spectrum(c->stream, k, dd, 0, lam, flg, nonpos, counts, floor_p);
+    square_vec(c->stream, k, lam, l1);
+    assemble(c->stream, n, k, d1, n, d2, n, l1, nullptr, 1, dd, floor_p, dV, 2 * n);
+    int64_t cnt[4];
+    BSE_CUDA(cudaMemcpyAsync(cnt, counts, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    BSE_CUDA(cudaStreamSynchronize(c->stream));
+    if (cnt[2] != 0)
+      throw DomainError{BSE_ERR_CONVERGENCE_FAILURE, 0, -1,
+                        "squared-problem spectrum has no positive eigenvalue"};
+    if (near_singular && cnt[0] > 0)
+      BSE_CUDA(cudaMemcpyAsync(near_singular, flg, sizeof(int64_t) * size_t(cnt[0]),
+                               cudaMemcpyDeviceToHost, c->stream));
+    if (n_near_singular) *n_near_singular = cnt[0];
+    BSE_CUDA(cudaMemcpyAsync(lambda, lam, sizeof(double) * size_t(k), cudaMemcpyDeviceToHost,
+                             c->stream));
     d2h(c, v, ldv, dV, 2 * n, 2 * n, k);
     BSE_CUDA(cudaStreamSynchronize(c->stream));
   });

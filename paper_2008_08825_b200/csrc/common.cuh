@@ -45,19 +45,22 @@ struct KernelTimer {
   int capacity = 0;
   int used = 0;
   int kind[4096];
-  double work[4096];  // flops (GEMM) or algorithmic bytes (panel) of each timed launch
+  double work[4096];   // flops (GEMM, complex-equivalent: 8 per complex MAC) or algorithmic
+                       // bytes (panel) of each timed launch
+  double work2[4096];  // GEMM: real flops the DMMA pipe executes (6 per complex MAC in 3M)
 };
 extern thread_local KernelTimer* g_timer;
 // Cap on the CTAs of the cooperative panel kernels (0 = every SM): the batch driver runs two
 // solves at once, each panel kernel on half of the SMs, so one solve's latency-bound panels
 // overlap the other's GEMM phases (set per calling thread from its context).
 extern thread_local int g_panel_ctas;
-inline int timer_begin(cudaStream_t s, int kind, double work) {
+inline int timer_begin(cudaStream_t s, int kind, double work, double work2 = -1.0) {
   KernelTimer* t = g_timer;
   if (!t || t->used + 2 > t->capacity || t->used / 2 >= 4096) return -1;
   const int slot = t->used / 2;
   t->kind[slot] = kind;
   t->work[slot] = work;
+  t->work2[slot] = work2 < 0.0 ? work : work2;
   cudaEventRecord(t->pool[t->used], s);
   t->used += 2;
   return slot;
