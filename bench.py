@@ -10,7 +10,7 @@ value = whole-job FP64 TFLOP/s under the reference flop model (160/3 n^3 real fl
 complex CHOL solve, proj/src/bench.cpp:41-50 x4 for complex). A CHOL+SVD sub-block times the
 paper's second method in the same run (its own throughput, latency and roofline).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 4096]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 4096]
                   [--method chol|chol-svd] [--lanes L] [--no-cpu-baseline] [--no-e2e]
                   [--no-chol-svd] [--v-gather]
 
@@ -133,7 +133,10 @@ def spawn_ranks(args) -> int:
         env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+           f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    # torch.distributed.run's parser would take "--n" as an abbreviation of its own options
+    cmd += ["--size" if a == "--n" else ("--size=" + a[4:] if a.startswith("--n=") else a)
+            for a in sys.argv[1:]]
     return subprocess.call(cmd, env=env)
 
 
@@ -175,13 +178,13 @@ class Dist:
     def all_gather_lams(self, local):
         """(k, n) eigenvalues of this rank's items -> (world, k, n) on every rank."""
         import torch
-        out = torch.empty((self.world,) + tuple(local.shape), dtype=local.dtype,
-                          device=local.device)
+        out = torch.empty((self.world * local.shape[0],) + tuple(local.shape[1:]),
+                          dtype=local.dtype, device=local.device)
         if self.dist:
             self.dist.all_gather_into_tensor(out, local.contiguous())
         else:
-            out[0].copy_(local)
-        return out
+            out.copy_(local)
+        return out.view((self.world,) + tuple(local.shape))
 
     def gather_v_to_rank0(self, vs, recv_buf):
         """Eigenvectors of one step (this rank's `lanes` 2n x n blocks) to rank 0 by
@@ -253,7 +256,7 @@ def run_reference(args):
         "s_per_solve": t / args.steps,
         "s_per_solve_median": statistics.median(times),
         "native_libs": sorted({os.path.basename(l.split()[-1]) for l in open("/proc/self/maps")
-                               if l.rstrip().endswith(".so") and "/bse" in l.split()[-1]}),
+                               if os.path.basename(l.split()[-1]).startswith("libbse")}),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -561,9 +564,9 @@ def run_ours(args, d: Dist):
     # solve / (time x GPUs x peak)); the Table-1 model figure is reported beside it
     dmma_per_solve = ph["gemm_dmma_flops"]
     fp64_exec_frac = dmma_per_solve * lanes * args.steps / (ms / 1e3) / 1e12 / peak64
-    # Cholesky phase (product_pair: A+-B and potrf of A-B, 4/3 n^3 complex = 16/3 n^3 real
-    # model flops) of a solve that owns the GPU
-    chol_tflops = (16.0 / 3.0) * n ** 3 / (ph_single["product_pair"] / 1e3) / 1e12
+    # Cholesky phase (product_pair: A+-B and potrf of A-B; zpotrf = n^3/6 complex MACs = 4/3 n^3
+    # real flops, SURVEY §8d per-phase counts) of a solve that owns the GPU
+    chol_tflops = (4.0 / 3.0) * n ** 3 / (ph_single["product_pair"] / 1e3) / 1e12
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -609,7 +612,7 @@ def run_ours(args, d: Dist):
             "cholesky_phase": {"ms": ph_single["product_pair"], "model_tflops": chol_tflops,
                                "frac_of_dmma_peak": chol_tflops / peak64,
                                "what": "A+-B and potrf(A-B) of one solve owning the GPU; "
-                                       "model flops 16/3 n^3 (complex potrf x4)"},
+                                       "model flops 4/3 n^3 (zpotrf)"},
             "phase_ms": {k: round(v, 3) for k, v in ph_single.items() if k in phase_keys},
             "phase_ms_batch_lane0": {k: round(v, 3) for k, v in ph.items() if k in phase_keys},
             "kernels": {"panel": {"ms": ph["panel_ms"], "launches": ph["panel_launches"],
@@ -643,7 +646,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=4096)
     ap.add_argument("--method", default="chol", choices=["chol", "chol-svd"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
