@@ -167,6 +167,16 @@ int bse_solve_batched_device(bse_ctx* ctx, int method, int64_t n, int64_t batch,
  * the SMs, so one solve's latency-bound reductions overlap another's GEMM phases. */
 int bse_ctx_set_batch_lanes(bse_ctx* ctx, int lanes);
 
+/* CHOL's certificate of A+B (product_pair, core.cpp:87-100). Default (0): A-B is factored
+ * (L, reused as in solvers.cpp:121) and A+B is certified by the spectrum of L^H (A+B) L,
+ * which is positive iff A+B is (Sylvester's law of inertia); the Cholesky of A+B runs only
+ * when that spectrum has an entry <= 0 or A-B failed, so NotDefinite{M1|M2}, its block and
+ * pivot are reported as the reference reports them. The two certificates can disagree only
+ * when lambda_min(A+B) is within rounding of zero. 1 = strict: the Cholesky of A+B runs on
+ * every CHOL solve, as the reference's product_pair does (one extra potrf, ~5% of a solve).
+ * Inherited by the context's batch lanes.                                                */
+int bse_ctx_set_strict_certificates(bse_ctx* ctx, int enable);
+
 /* ---------------------------------------------------------------- core glue (core.cpp) */
 /* product_pair (core.cpp:87-100): m1 = a+b, m2 = a-b, each certified by Cholesky.     */
 int bse_product_pair(bse_ctx* ctx, int64_t n, const double* a, int64_t lda,

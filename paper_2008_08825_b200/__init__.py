@@ -253,6 +253,11 @@ class Context:
         _lib.lib().bse_ctx_last_phase_times(self._h, ctypes.byref(t))
         return {k: getattr(t, k) for k, _ in PhaseTimes._fields_}
 
+    def set_strict_certificates(self, enable: bool = True):
+        """CHOL: certify A+B by its own Cholesky on every solve, as the reference's
+        product_pair does (bse_ctx_set_strict_certificates)."""
+        _lib.lib().bse_ctx_set_strict_certificates(self._h, 1 if enable else 0)
+
     def set_kernel_timing(self, enable: bool = True):
         _lib.lib().bse_ctx_set_kernel_timing(self._h, 1 if enable else 0)
 

@@ -54,6 +54,7 @@ SYMBOLS = {
     "bse_solve_batched_device": (c_int, [c_dp, c_int, c_i64, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp,
                                          c_dp, c_i64, c_dp, c_dp, c_dp, ctypes.POINTER(Status)]),
     "bse_ctx_set_batch_lanes": (c_int, [c_dp, c_int]),
+    "bse_ctx_set_strict_certificates": (c_int, [c_dp, c_int]),
     "bse_set_tridiagonal_reduction": (c_int, [c_int]),
     "bse_product_pair": (c_int, [c_dp, c_i64, c_dp, c_i64, c_dp, c_i64, c_dp, c_dp,
                                  ctypes.POINTER(Status)]),

@@ -27,11 +27,11 @@ template <bool CA, bool CB>
 void launch_z(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   using T = ZGemmTile<kBM, kBN, kBK, kWM, kWN, kST, CA, CB>;
   auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWN, kST, CA, CB>;
-  static const bool configured = [&] {  // one-time setup per template instance (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
     return true;
-  }();
+  });
   (void)configured;
   kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
   BSE_LAUNCH_CHECK();
@@ -46,11 +46,11 @@ template <bool CA, bool CB>
 void launch_z_short(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   using T = ZGemmTile<kBM, kBN, kBK, kWM, kWNs, kSTs, CA, CB>;
   auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWNs, kSTs, CA, CB, kMinBs>;
-  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
     return true;
-  }();
+  });
   (void)configured;
   kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
   BSE_LAUNCH_CHECK();
@@ -62,11 +62,11 @@ template <int BN, int BK, int ST, int MINB, bool CA, bool CB>
 void launch_z_3m_cfg(cudaStream_t s, const ZGemmParams& p, dim3 grid) {
   using T = ZGemmTile<kBM, BN, BK, kWM, kWNs, ST, CA, CB>;
   auto kern = zgemm_dmma_kernel<kBM, BN, BK, kWM, kWNs, ST, CA, CB, MINB, true>;
-  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
     return true;
-  }();
+  });
   (void)configured;
   kern<<<grid, T::NTHREADS, T::SMEM, s>>>(p);
   BSE_LAUNCH_CHECK();
@@ -229,11 +229,11 @@ void dgemm_nn(cudaStream_t s, int64_t m, int64_t n, int64_t k, double alpha, con
   constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, ST = 3;
   using T = DGemmTile<BM, BN, BK, WM, WN, ST>;
   auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, ST>;
-  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(T::SMEM)));
     return true;
-  }();
+  });
   (void)configured;
   DGemmParams p{};
   p.m = m; p.n = n; p.k = k;
@@ -296,11 +296,11 @@ __global__ void __launch_bounds__(256) ztrtri_diag_kernel(int64_t n, const z_t* 
 void ztrtri_diag_blocks(cudaStream_t s, int64_t n, const z_t* L, int64_t ldl, int nb, z_t* inv) {
   const int64_t nblk = ceil_div(n, nb);
   const size_t smem = size_t(2) * nb * (nb + 1) * sizeof(z_t);
-  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(ztrtri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
     return true;
-  }();
+  });
   (void)configured;
   ztrtri_diag_kernel<<<unsigned(nblk), 256, smem, s>>>(n, L, ldl, nb, inv);
   BSE_LAUNCH_CHECK();

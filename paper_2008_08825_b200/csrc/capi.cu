@@ -4,6 +4,7 @@
 // solvers.hpp, types.hpp) onto plain pointers + status codes. Host-pointer entry points
 // stage through the context's device arena; nothing here ever computes on the CPU: when
 // no CUDA device is present every compute entry point fails with BSE_ERR_NO_DEVICE.
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <thread>
@@ -147,11 +148,14 @@ void d2h(bse_ctx* c, double* dst, int64_t ldd, const z_t* src, int64_t lds, int6
 const z_t kOne = {1.0, 0.0}, kZero = {0.0, 0.0};
 
 // Solve with device-resident buffers carved from a separate allocation (the solver pipeline
-// owns the arena). Kept simple: per-call cudaMallocAsync on the context stream.
+// owns the arena): stream-ordered allocations from the context's private memory pool (kept
+// mapped between calls; bse_ctx_release_workspace trims it).
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t s;
-  DevBuf(size_t bytes, cudaStream_t st) : s(st) { BSE_CUDA(cudaMallocAsync(&p, bytes, s)); }
+  DevBuf(size_t bytes, bse_ctx* c) : s(c->stream) {
+    BSE_CUDA(cudaMallocFromPoolAsync(&p, bytes, c->pool, s));
+  }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, s);
   }
@@ -227,11 +231,15 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
     for (auto& st2 : c->la) BSE_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     for (auto& ev : c->la_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : c->batch_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    // keep the stream-ordered staging buffers of bse_solve mapped between calls
-    cudaMemPool_t pool;
-    BSE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    // a private pool for the stream-ordered staging buffers, kept mapped between calls (the
+    // process-wide default pool and its release threshold are left to the application)
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    BSE_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t keep = UINT64_MAX;
-    BSE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    BSE_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
     for (auto& ev : c->sink_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : c->ev) BSE_CUDA(cudaEventCreate(&ev));
   } catch (const CudaError& ex) {
@@ -278,6 +286,7 @@ int bse_ctx_destroy(bse_ctx* c) {
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   delete c;
   return BSE_OK;
 }
@@ -312,12 +321,15 @@ int bse_ctx_set_kernel_timing(bse_ctx* c, int enable) {
 
 int bse_ctx_release_workspace(bse_ctx* c) {
   if (!c) return BSE_OK;
+  for (bse_ctx* t : c->twin)  // the batch lanes' arenas and pools too
+    if (t) bse_ctx_release_workspace(t);
   std::lock_guard<std::mutex> lock(c->mu);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->arena) cudaFree(c->arena);
   c->arena = nullptr;
   c->arena_bytes = 0;
+  if (c->pool) cudaMemPoolTrimTo(c->pool, 0);
   return BSE_OK;
 }
 
@@ -347,7 +359,7 @@ int bse_solve(bse_ctx* c, int method, int64_t n, const double* a, int64_t lda, c
     if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
     const size_t nn = size_t(n) * size_t(n);
     DevBuf buf(nn * 2 * sizeof(z_t) + 2 * nn * sizeof(z_t) + size_t(n) * sizeof(double) + 1024,
-               c->stream);
+               c);
     z_t* dA = buf.as<z_t>();
     z_t* dB = dA + nn;
     z_t* dV = dB + nn;
@@ -449,7 +461,7 @@ void run_lane(bse_ctx* c, const BatchIO& io, const std::vector<int64_t>& items, 
   }
   const size_t nn = size_t(n) * size_t(n);
   const size_t slot = 2 * nn + 2 * nn + size_t(n) / 2 + 64;  // in z_t units
-  DevBuf buf(2 * slot * sizeof(z_t), c->stream);
+  DevBuf buf(2 * slot * sizeof(z_t), c);
   z_t *dA[2], *dB[2], *dV[2];
   double* dL[2];
   for (int k = 0; k < 2; ++k) {
@@ -542,18 +554,36 @@ void run_batch(bse_ctx* c, const BatchIO& io, int64_t batch, int64_t* failed_ind
     int v;
     ~Restore() { g_panel_ctas = v; }
   } restore{prev_cap};
-  BatchFail fail;
-  std::vector<std::thread> extra;
-  std::vector<std::exception_ptr> lane_err(static_cast<size_t>(lanes));
+  // every lane context exists before any lane thread starts: a failing create throws here,
+  // with no thread running
   for (int l = 1; l < lanes; ++l) {
     if (!c->twin[l - 1]) {
       bse_status st{};
       if (bse_ctx_create(&c->twin[l - 1], c->device, &st) != BSE_OK)
         throw std::runtime_error(std::string("batch lane context: ") + st.message);
     }
+  }
+  BatchFail fail;
+  std::vector<std::exception_ptr> lane_err(static_cast<size_t>(lanes));
+  std::vector<std::thread> extra;
+  extra.reserve(size_t(lanes));
+  // joins every started lane thread on every exit path (a std::thread that is still joinable
+  // when destroyed terminates the process, and the lanes reference this frame's locals)
+  struct JoinAll {
+    std::vector<std::thread>& t;
+    BatchFail& f;
+    ~JoinAll() {
+      if (std::any_of(t.begin(), t.end(), [](const std::thread& x) { return x.joinable(); }))
+        f.first.store(-1);  // an early exit: lanes stop at their next item
+      for (auto& x : t)
+        if (x.joinable()) x.join();
+    }
+  } join_all{extra, fail};
+  const int cap = g_panel_ctas;             // set above from `lanes`
+  const int tmode = current_tridiag_mode();  // the caller's snapshot, for every lane
+  for (int l = 1; l < lanes; ++l) {
     bse_ctx* lc = c->twin[l - 1];
-    const int cap = g_panel_ctas;  // set above from `lanes`
-    const int tmode = current_tridiag_mode();  // the caller's snapshot, for every lane
+    lc->strict_m1 = c->strict_m1;
     extra.emplace_back([&, l, lc, cap, tmode] {
       const TridiagModeScope tridiag_mode(tmode);
       try {
@@ -624,6 +654,13 @@ int bse_solve_batched_device(bse_ctx* c, int method, int64_t n, int64_t batch,
 
 int bse_set_tridiagonal_reduction(int mode) { return bseg::set_tridiag_mode(mode); }
 
+int bse_ctx_set_strict_certificates(bse_ctx* c, int enable) {
+  if (!c) return BSE_ERR_INVALID_SPEC;
+  std::lock_guard<std::mutex> lock(c->mu);
+  c->strict_m1 = enable != 0;
+  return BSE_OK;
+}
+
 int bse_ctx_set_batch_lanes(bse_ctx* c, int lanes) {
   if (!c || lanes < 1 || lanes > 8) return BSE_ERR_INVALID_SPEC;
   std::lock_guard<std::mutex> lock(c->mu);
@@ -636,7 +673,7 @@ int bse_product_pair(bse_ctx* c, int64_t n, const double* a, int64_t lda, const 
   return guarded(c, st, [&] {
     check_dims(n, lda, ldb);
     const size_t nn = size_t(n) * size_t(n);
-    DevBuf buf(nn * 5 * sizeof(z_t) + 64 * 64 * sizeof(z_t) + 64, c->stream);
+    DevBuf buf(nn * 5 * sizeof(z_t) + 64 * 64 * sizeof(z_t) + 64, c);
     z_t* dA = buf.as<z_t>();
     z_t* dB = dA + nn;
     z_t* dM1 = dB + nn;
@@ -683,7 +720,7 @@ int bse_assemble_eigenvectors(bse_ctx* c, int64_t n, int64_t k, const double* v1
     }
     if (n == 0 || k == 0) return;
     const size_t nk = size_t(n) * size_t(k);
-    DevBuf buf(nk * 4 * sizeof(z_t) + 2 * size_t(k) * sizeof(double) + 64, c->stream);
+    DevBuf buf(nk * 4 * sizeof(z_t) + 2 * size_t(k) * sizeof(double) + 64, c);
     z_t* d1 = buf.as<z_t>();
     z_t* d2 = d1 + nk;
     z_t* dV = d2 + nk;
@@ -709,7 +746,7 @@ int bse_assemble_from_squares(bse_ctx* c, int64_t n, int64_t k, const double* v1
     const size_t nk = size_t(n) * size_t(k);
     DevBuf buf(nk * 4 * sizeof(z_t) + 3 * size_t(k) * sizeof(double) +
                    2 * size_t(k) * sizeof(int64_t) + 8 * sizeof(int64_t) + 64,
-               c->stream);
+               c);
     z_t* d1 = buf.as<z_t>();
     z_t* d2 = d1 + nk;
     z_t* dV = d2 + nk;
@@ -750,7 +787,7 @@ int bse_cholesky_lower(bse_ctx* c, int64_t n, const double* m, int64_t ldm, doub
     if (n < 1 || ldm < n || ldl < n)
       throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "cholesky_lower: bad dimensions"};
     const size_t nn = size_t(n) * size_t(n);
-    DevBuf buf(nn * sizeof(z_t) + 64 * 64 * sizeof(z_t) + 64, c->stream);
+    DevBuf buf(nn * sizeof(z_t) + 64 * 64 * sizeof(z_t) + 64, c);
     z_t* dM = buf.as<z_t>();
     z_t* ws = dM + nn;
     int* info = reinterpret_cast<int*>(ws + 64 * 64);
@@ -792,7 +829,7 @@ int bse_matmul(bse_ctx* c, int64_t ar, int64_t ac, const double* a, int64_t lda,
     if (am == 0 || bn == 0) return;
     const size_t na = size_t(ar) * size_t(ac), nb = size_t(br) * size_t(bc),
                  ncm = size_t(am) * size_t(bn);
-    DevBuf buf((na + nb + ncm) * sizeof(z_t) + 64, c->stream);
+    DevBuf buf((na + nb + ncm) * sizeof(z_t) + 64, c);
     z_t* dA = buf.as<z_t>();
     z_t* dB = dA + na;
     z_t* dC = dB + nb;
@@ -826,7 +863,7 @@ int bse_tri_solve(bse_ctx* c, int64_t n, const double* l, int64_t ldl, int64_t r
     if (rows == 0 || cols == 0) return;
     const size_t nn = size_t(n) * size_t(n), nr = size_t(rows) * size_t(cols);
     const int64_t other = side == BSE_SIDE_LEFT ? cols : rows;
-    DevBuf buf((nn + nr + trsm_workspace_elems(n, other, 64)) * sizeof(z_t) + 64, c->stream);
+    DevBuf buf((nn + nr + trsm_workspace_elems(n, other, 64)) * sizeof(z_t) + 64, c);
     z_t* dL = buf.as<z_t>();
     z_t* dX = dL + nn;
     z_t* ws = dX + nr;

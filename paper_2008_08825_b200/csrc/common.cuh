@@ -2,6 +2,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <mutex>
+#include <stdexcept>
 #include <stdint.h>
 
 #include <cmath>
@@ -68,6 +71,23 @@ inline int timer_begin(cudaStream_t s, int kind, double work, double work2 = -1.
 inline void timer_end(cudaStream_t s, int slot) {
   if (slot < 0 || !g_timer) return;
   cudaEventRecord(g_timer->pool[2 * slot + 1], s);
+}
+
+// One-time setup per CUDA device: kernel attributes (the dynamic shared-memory limit) and
+// occupancy queries are per device, so a process that runs solves on several devices (one
+// context per device, or batch lanes on the same device from several host threads) sets them
+// up once for each device. Every call site instantiates its own storage (the lambda's type).
+constexpr int kMaxDevices = 64;
+template <typename F>
+const auto& per_device(F&& setup) {
+  using T = decltype(setup());
+  static std::once_flag once[kMaxDevices];
+  static T value[kMaxDevices];
+  int dev = 0;
+  BSE_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("device index out of range");
+  std::call_once(once[dev], [&] { value[dev] = setup(); });
+  return value[dev];
 }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

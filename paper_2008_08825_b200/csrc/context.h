@@ -10,6 +10,8 @@
 struct bse_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  bool strict_m1 = false;  // CHOL: certify A+B by its own Cholesky on every solve (see solvers.cu)  // stream-ordered staging buffers (DevBuf, batch staging)
   void* arena = nullptr;
   size_t arena_bytes = 0;
   int64_t launches = 0;

@@ -566,7 +566,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
   struct Occ {
     int blocks_per_sm, num_sms;
   };
-  static const Occ occ = [&] {  // one-time setup (thread-safe: batch lanes)
+  const Occ& occ = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     Occ o{0, 0};
     BSE_CUDA(cudaFuncSetAttribute(hetrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
@@ -576,7 +576,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     BSE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.blocks_per_sm, hetrd_panel_kernel,
                                                            kThreads, smem));
     return o;
-  }();
+  });
   const int blocks_per_sm = occ.blocks_per_sm, num_sms = occ.num_sms;
   if (blocks_per_sm < 1) throw std::runtime_error("hetrd: kernel cannot be resident");
   if (n == 1) {

@@ -658,13 +658,13 @@ void zhetrd_2stage(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, do
   Ws2 w = carve(ws, n);
   const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
   BSE_CUDA(cudaMemsetAsync(tau1, 0, sizeof(z_t) * size_t(n), s));
-  static const bool attr = [] {  // one-time setup (thread-safe: batch lanes)
+  const bool& attr = per_device([] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(chase_smem())));
     BSE_CUDA(cudaFuncSetAttribute(he2hb_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kQrSmem)));
     return true;
-  }();
+  });
   (void)attr;
   // ---- stage 1: panels c0 = 0, kB, ... while the panel has >= 2 rows below the band
   for (int64_t c0 = 0; c0 + kB <= n - 2; c0 += kB) {

@@ -239,11 +239,11 @@ void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z
   unsigned* loaded = reinterpret_cast<unsigned*>(ws);
   const size_t smem = size_t(kNB * kLD + 3 * kNB + kNB * (kPR + 1)) * sizeof(z_t) +
                       kNB * sizeof(double);
-  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(zpotrf_panel_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     return true;
-  }();
+  });
   (void)configured;
   BSE_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), s));
   BSE_CUDA(cudaMemsetAsync(loaded, 0, sizeof(unsigned), s));

@@ -201,6 +201,11 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
       throw DomainError{BSE_ERR_NOT_DEFINITE, BSE_BLOCK_M2, int64_t(h) - 1,
                         "A-B is not positive definite: " + pivot_msg(h)};
     }
+    // strict certificates (bse_ctx_set_strict_certificates): the Cholesky of A+B on every
+    // solve, exactly as product_pair does (core.cpp:89-93). The default certifies A+B from
+    // the spectrum of L^H (A+B) L below (Sylvester's inertia: positive iff A+B is), which
+    // can only differ from zpotrf's verdict when lambda_min(A+B) is within rounding of 0.
+    if (c->strict_m1) certify_m1(c, n, A, lda, B, ldb, b2, b3, info + 0, ws_potrf2);
   }
   clk.mark();
   // M = L^H M1 L  (solvers.cpp:122-123), lower triangle only (zheevd reads 'L'), in the
@@ -229,7 +234,8 @@ void solve_chol_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const z_t*
     BSE_CUDA(cudaStreamSynchronize(s));
     // M1 is certified by the spectrum when its smallest eigenvalue is positive; otherwise
     // factor it (b2, b3 are free here) and report NotDefinite{M1} as the reference would
-    if (h != 0 || !(dmin > 0.0)) certify_m1(c, n, A, lda, B, ldb, b3, b2, info + 0, ws_potrf2);
+    if (!c->strict_m1 && (h != 0 || !(dmin > 0.0)))
+      certify_m1(c, n, A, lda, B, ldb, b3, b2, info + 0, ws_potrf2);
     if (h != 0)
       throw DomainError{BSE_ERR_CONVERGENCE_FAILURE, 0, -1,
                         "zheevd failed to converge (info=" + std::to_string(h) + ")"};

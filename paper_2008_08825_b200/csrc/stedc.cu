@@ -841,8 +841,8 @@ size_t stedc_workspace_bytes(int64_t n) {
   b += nn * sizeof(double) * 3;          // Qalt, UT, UB
   b += size_t(n) * sizeof(double) * 8;   // D, E, dl, w, defval, tau, what, scale
   b += size_t(n) * sizeof(int) * 13;     // index arrays
-  b += size_t(n) * (sizeof(MergeDesc) + sizeof(MergeState)) + 4096;
-  b += size_t(2 * n + 2) * sizeof(int);  // tile offsets
+  b += size_t(2 * n + 2) * sizeof(MergeDesc) + size_t(n) * sizeof(MergeState) + 4096;
+  b += size_t(4 * n + 130) * sizeof(int);  // tile offsets of every level
   return b + 64 * 16;
 }
 
@@ -884,9 +884,9 @@ void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, vo
   int* acolT = carve<int>(p, 2 * n);
   int* acolB = carve<int>(p, n);
   int* ccol = carve<int>(p, n);
-  MergeDesc* mdesc = carve<MergeDesc>(p, n);
+  MergeDesc* mdesc_all = carve<MergeDesc>(p, 2 * n + 2);  // every level's merges
   MergeState* mstate = carve<MergeState>(p, n);
-  int* tile_off = carve<int>(p, 2 * n + 2);
+  int* tile_off_all = carve<int>(p, 4 * n + 130);
 
   stedc_scale_kernel<<<1, 1024, 0, s>>>(n, d, e, D, E, scale);
   BSE_LAUNCH_CHECK();
@@ -905,37 +905,55 @@ void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, vo
   stedc_leaf_kernel<<<unsigned(ceil_div(nleaf, 4)), 128, 0, s>>>(n, L, D, E, bufs[cur], d_info);
   BSE_LAUNCH_CHECK();
 
-  std::vector<MergeDesc> hmd;
-  std::vector<int> htile;
-  static const bool configured = [&] {  // one-time setup (thread-safe: batch lanes)
+  const bool& configured = per_device([&] {  // one-time setup per device (thread-safe: batch lanes)
     BSE_CUDA(cudaFuncSetAttribute(stedc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(GT::SMEM)));
     return true;
-  }();
+  });
   (void)configured;
+  // Every level's merge descriptors and GEMM tile offsets are built up front and go to the
+  // device in one copy each (no host synchronisation inside the tree).
+  std::vector<MergeDesc> hmd;
+  std::vector<int> htile;
+  std::vector<int> lvl_md(size_t(std::max(L, 1))), lvl_tile(size_t(std::max(L, 1))),
+      lvl_maxn(size_t(std::max(L, 1)));
   for (int lvl = L - 1; lvl >= 0; --lvl) {
     const int nm = 1 << lvl;
-    hmd.resize(nm);
-    htile.assign(2 * nm + 1, 0);
+    const int md0 = int(hmd.size()), t0 = int(htile.size());
+    lvl_md[size_t(lvl)] = md0;
+    lvl_tile[size_t(lvl)] = t0;
+    htile.resize(size_t(t0 + 2 * nm + 1), 0);
     int maxN = 0;
     for (int m = 0; m < nm; ++m) {
       const int64_t a = (int64_t(m) * n) >> lvl;
       const int64_t mid = (int64_t(2 * m + 1) * n) >> (lvl + 1);
       const int64_t b = (int64_t(m + 1) * n) >> lvl;
-      hmd[m] = MergeDesc{int(a), int(mid - a), int(b - mid)};
+      hmd.push_back(MergeDesc{int(a), int(mid - a), int(b - mid)});
       maxN = std::max<int>(maxN, int(b - a));
     }
+    lvl_maxn[size_t(lvl)] = maxN;
     for (int m = 0; m < nm; ++m) {
-      const int N = hmd[m].n1 + hmd[m].n2;
+      const MergeDesc& q = hmd[size_t(md0 + m)];
+      const int N = q.n1 + q.n2;
       const int tn = (N + gBN - 1) / gBN;
-      htile[2 * m + 1] = htile[2 * m] + ((hmd[m].n1 + gBM - 1) / gBM) * tn;
-      htile[2 * m + 2] = htile[2 * m + 1] + ((hmd[m].n2 + gBM - 1) / gBM) * tn;
+      htile[size_t(t0 + 2 * m + 1)] = htile[size_t(t0 + 2 * m)] + ((q.n1 + gBM - 1) / gBM) * tn;
+      htile[size_t(t0 + 2 * m + 2)] = htile[size_t(t0 + 2 * m + 1)] + ((q.n2 + gBM - 1) / gBM) * tn;
     }
-    // descriptors are tiny; a pageable async copy is fine and keeps the stream order
-    BSE_CUDA(cudaMemcpyAsync(mdesc, hmd.data(), sizeof(MergeDesc) * nm, cudaMemcpyHostToDevice, s));
-    BSE_CUDA(cudaMemcpyAsync(tile_off, htile.data(), sizeof(int) * (2 * nm + 1),
+  }
+  if (L > 0) {
+    if (hmd.size() > size_t(2 * n + 2) || htile.size() > size_t(4 * n + 130))
+      throw std::runtime_error("stedc: level descriptors exceed the workspace");
+    // pageable sources: the copies are staged before cudaMemcpyAsync returns
+    BSE_CUDA(cudaMemcpyAsync(mdesc_all, hmd.data(), sizeof(MergeDesc) * hmd.size(),
                              cudaMemcpyHostToDevice, s));
-    BSE_CUDA(cudaStreamSynchronize(s));  // host vectors are reused next level
+    BSE_CUDA(cudaMemcpyAsync(tile_off_all, htile.data(), sizeof(int) * htile.size(),
+                             cudaMemcpyHostToDevice, s));
+  }
+  for (int lvl = L - 1; lvl >= 0; --lvl) {
+    const int nm = 1 << lvl;
+    const int maxN = lvl_maxn[size_t(lvl)];
+    MergeDesc* mdesc = mdesc_all + lvl_md[size_t(lvl)];
+    const int* tile_off = tile_off_all + lvl_tile[size_t(lvl)];
     StedcLevel lv{};
     lv.md = mdesc; lv.ms = mstate; lv.nmerge = nm; lv.n = n;
     lv.D = D; lv.E = E; lv.Qold = bufs[cur]; lv.Qnew = bufs[cur ^ 1];
@@ -961,7 +979,7 @@ void dstedc(cudaStream_t s, int64_t n, double* d, const double* e, double* Q, vo
     BSE_LAUNCH_CHECK();
     stedc_u_kernel<<<gw, 32 * wpb, 0, s>>>(lv);
     BSE_LAUNCH_CHECK();
-    const int tiles = htile[2 * nm];
+    const int tiles = htile[size_t(lvl_tile[size_t(lvl)] + 2 * nm)];
     stedc_gemm_kernel<<<unsigned(tiles), GT::NTHREADS, GT::SMEM, s>>>(lv, tile_off);
     BSE_LAUNCH_CHECK();
     stedc_finish_kernel<<<dim3(unsigned(std::min(maxN, 1024)), unsigned(nm)), 128, 0, s>>>(lv);
