@@ -18,6 +18,10 @@ namespace bseg {
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local KernelTimer* g_timer = nullptr;
 thread_local int g_panel_ctas = 0;
+int panel_cta_cap() {
+  static const int solo = getenv("BSE_SOLO_PANEL_CTAS") ? atoi(getenv("BSE_SOLO_PANEL_CTAS")) : 0;
+  return g_panel_ctas > 0 ? g_panel_ctas : solo;
+}
 
 namespace {
 
@@ -411,6 +415,10 @@ void ztrsm_lower(cudaStream_t s, int side, int op, int64_t n, int64_t other, con
 }
 
 CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n) {
+  return make_tile_map_box(A, lda, n, kRingT, kRingT);
+}
+
+CUtensorMap make_tile_map_box(const z_t* A, int64_t lda, int64_t n, int box_rows, int box_cols) {
   static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {  // thread-safe one-time lookup
     PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -423,7 +431,7 @@ CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n) {
   CUtensorMap map;
   const cuuint64_t dims[2] = {cuuint64_t(2 * n), cuuint64_t(n)};
   const cuuint64_t strides[1] = {cuuint64_t(lda) * sizeof(z_t)};
-  const cuuint32_t box[2] = {128, 64};
+  const cuuint32_t box[2] = {cuuint32_t(2 * box_rows), cuuint32_t(box_cols)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<z_t*>(A), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

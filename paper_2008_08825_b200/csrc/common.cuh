@@ -57,6 +57,9 @@ extern thread_local KernelTimer* g_timer;
 // solves at once, each panel kernel on half of the SMs, so one solve's latency-bound panels
 // overlap the other's GEMM phases (set per calling thread from its context).
 extern thread_local int g_panel_ctas;
+// The cap in force for this thread's panel launches: the batch lane's, else the developer
+// switch BSE_SOLO_PANEL_CTAS (a single solve's panels on fewer SMs, to trace a lane's panel).
+int panel_cta_cap();
 inline int timer_begin(cudaStream_t s, int kind, double work, double work2 = -1.0) {
   KernelTimer* t = g_timer;
   if (!t || t->used + 2 > t->capacity || t->used / 2 >= 4096) return -1;

@@ -629,7 +629,7 @@ void zgebrd_upper(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     const int64_t m = n - p0;
     const int64_t tiles = ceil_div(m, kT) * ceil_div(m, kT);
     int G = int(min64(int64_t(blocks_per_sm) * num_sms, tiles));
-    if (g_panel_ctas > 0) G = int(min64(G, g_panel_ctas));  // batch lanes share the SMs
+    if (panel_cta_cap() > 0) G = int(min64(G, panel_cta_cap()));  // batch lanes share the SMs
     G = max(G, 1);
     {
       const int64_t K = nch - p0 / kT;

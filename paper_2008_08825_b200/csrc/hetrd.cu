@@ -270,23 +270,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       const z_t* tl = ring.slot(k % kRing);
       const z_t v0 = vr[lane], v1 = vr[lane + 32];
       z_t r0 = zero, r1 = zero, pc[8];
+      if (!diag) {  // (CTA-uniform branch) the bulk of the sweep: no masks
+        const z_t* tw = tl + ring_idx(lane, 8 * warp);
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const int c = 8 * warp + cc;
-        const z_t a0 = tl[ring_idx(lane, c)], a1 = tl[ring_idx(lane + 32, c)];
-        // diagonal tiles: lower triangle only, the Hermitian diagonal real (selects, no
-        // branch: one copy of the loop body keeps the sweep's code small)
-        const bool low0 = !diag || lane > c, low1 = !diag || lane + 32 > c;
-        const bool dg0 = diag && lane == c, dg1 = diag && lane + 32 == c;
-        const z_t ac0 = low0 ? a0 : zero, ac1 = low1 ? a1 : zero;
-        const z_t ar0 = low0 ? a0 : (dg0 ? make_double2(a0.x, 0.0) : zero);
-        const z_t ar1 = low1 ? a1 : (dg1 ? make_double2(a1.x, 0.0) : zero);
-        const z_t vcc = vc[c];
-        zfma(r0, ar0, vcc);
-        zfma(r1, ar1, vcc);
-        pc[cc] = zero;
-        zcfma(pc[cc], ac0, v0);
-        zcfma(pc[cc], ac1, v1);
+        for (int cc = 0; cc < 8; ++cc) {
+          const z_t a0 = tw[cc * kRingT], a1 = tw[cc * kRingT + 32];
+          const z_t vcc = vc[8 * warp + cc];
+          zfma(r0, a0, vcc);
+          zfma(r1, a1, vcc);
+          pc[cc] = zcmul(a0, v0);
+          zcfma(pc[cc], a1, v1);
+        }
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const int c = 8 * warp + cc;
+          const z_t a0 = tl[ring_idx(lane, c)], a1 = tl[ring_idx(lane + 32, c)];
+          // diagonal tiles: lower triangle only, the Hermitian diagonal real
+          const bool low0 = lane > c, low1 = lane + 32 > c;
+          const z_t ac0 = low0 ? a0 : zero, ac1 = low1 ? a1 : zero;
+          const z_t ar0 = low0 ? a0 : (lane == c ? make_double2(a0.x, 0.0) : zero);
+          const z_t ar1 = low1 ? a1 : (lane + 32 == c ? make_double2(a1.x, 0.0) : zero);
+          const z_t vcc = vc[c];
+          zfma(r0, ar0, vcc);
+          zfma(r1, ar1, vcc);
+          pc[cc] = zero;
+          zcfma(pc[cc], ac0, v0);
+          zcfma(pc[cc], ac1, v1);
+        }
       }
       const z_t ctot = warp_transpose_zsum8(pc);
       z_t* rowred = swp + (j & 1) * (8 * kT + kT);  // [8 warps][64 rows] | [64 cols]
@@ -597,7 +608,7 @@ void zhetrd_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, double* d, dou
     const int64_t m = n - p0;
     const int64_t tiles = ceil_div(m, kT) * (ceil_div(m, kT) + 1) / 2;
     int G = int(min64(min64(int64_t(blocks_per_sm) * num_sms, 256), tiles));  // phase B: G <= 256
-    if (g_panel_ctas > 0) G = int(min64(G, g_panel_ctas));  // batch lanes share the SMs
+    if (panel_cta_cap() > 0) G = int(min64(G, panel_cta_cap()));  // batch lanes share the SMs
     G = max(G, 1);
     {
       const int64_t K = nch - (p0 + 1) / kT;

@@ -56,6 +56,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // Host: tensor map for a column-major complex n x n matrix (see the header comment).
 CUtensorMap make_tile_map(const z_t* A, int64_t lda, int64_t n);
+// The same view with a box_rows x box_cols complex box (slot layout c * box_rows + r).
+CUtensorMap make_tile_map_box(const z_t* A, int64_t lda, int64_t n, int box_rows, int box_cols);
 
 template <int kSlots>
 struct TileRing {
