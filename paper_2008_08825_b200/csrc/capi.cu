@@ -222,13 +222,23 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
   c->device = device;
   try {
     BSE_CUDA(cudaSetDevice(device));
-    BSE_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    BSE_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    // Stream priorities: the solve's critical chains (c->stream, c->aux: Cholesky panels, the
+    // reduction panels, the divide & conquer) run at the highest priority, the Cholesky
+    // look-ahead streams (bulk trailing HERK updates) at the lowest, so a panel launched while
+    // a bulk update fills the GPU takes the next free SMs instead of queueing behind the
+    // update's remaining CTAs (BSE_STREAM_PRIORITIES=0: all equal, A/B switch).
+    static const bool prio = !getenv("BSE_STREAM_PRIORITIES") || atoi(getenv("BSE_STREAM_PRIORITIES")) != 0;
+    int lo_prio = 0, hi_prio = 0;
+    BSE_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    if (!prio) lo_prio = hi_prio = 0;
+    BSE_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_prio));
+    BSE_CUDA(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, hi_prio));
     BSE_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     BSE_CUDA(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     BSE_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     BSE_CUDA(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
-    for (auto& st2 : c->la) BSE_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    for (auto& st2 : c->la)
+      BSE_CUDA(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, lo_prio));
     for (auto& ev : c->la_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : c->batch_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     // a private pool for the stream-ordered staging buffers, kept mapped between calls (the

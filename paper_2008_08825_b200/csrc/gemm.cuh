@@ -87,8 +87,24 @@ __global__ void __launch_bounds__(ZGemmTile<BM, BN, BK, WM, WN, STAGES, CONJ_A, 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   z_t* smem = reinterpret_cast<z_t*>(smem_raw);
 
-  const int64_t m0 = int64_t(blockIdx.x) * BM;
-  const int64_t n0 = int64_t(blockIdx.y) * BN;
+  // Grouped rasterisation: the hardware dispatches CTAs x-fastest, so consecutive CTAs walk
+  // down a group of kGroupM tile rows before moving to the next tile column. The CTAs in
+  // flight then share A row panels and B column panels in L2 (instead of every resident
+  // tile column re-streaming all of A from HBM).
+  constexpr int kGroupM = 16;
+  int bm = blockIdx.x, bn = blockIdx.y;
+  {
+    const int tm = gridDim.x, tn = gridDim.y;
+    const int lin = blockIdx.y * tm + blockIdx.x;
+    const int per_group = kGroupM * tn;
+    const int first = (lin / per_group) * kGroupM;
+    const int gsz = min(tm - first, kGroupM);
+    const int r = lin % per_group;
+    bm = first + r % gsz;
+    bn = r / gsz;
+  }
+  const int64_t m0 = int64_t(bm) * BM;
+  const int64_t n0 = int64_t(bn) * BN;
   if (p.c_lower && m0 + BM <= n0) return;  // tile strictly above the diagonal
 
   const z_t* A = p.A;
