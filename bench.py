@@ -547,7 +547,7 @@ def run_ours(args, d: Dist):
 
     # ---- rooflines: the reduction panel against HBM and the DMMA GEMMs against the FP64
     # tensor peak, both from the live event timings (lane 0 in the timed region, and a solve
-    # that owns the GPU); `roofline` is the class with the larger share of lane 0's time
+    # that owns the GPU); `roofline` is the class with the larger share of a solve's time
     peaks = load_json("MEASURED_PEAKS.json")
     traffic = load_json("profiles", "traffic.json")
     peak64, peak64_src = fp64_peak()
@@ -558,7 +558,9 @@ def run_ours(args, d: Dist):
     rf_gemm = roofline_gemm(ph, peak64, peak64_src, lane_where, traffic)
     rf_panel_w = roofline_panel(ph_single, method, peaks, whole_where, traffic)
     rf_gemm_w = roofline_gemm(ph_single, peak64, peak64_src, whole_where, traffic)
-    roofline = rf_panel if ph["panel_ms"] >= ph["gemm_ms"] else rf_gemm
+    # the dominant class is chosen on the solve that owns the GPU (CHOL: panel ~59 ms vs GEMMs
+    # ~51 ms; in the lanes the two are within noise of each other and would flip run to run)
+    roofline = rf_panel if ph_single["panel_ms"] >= ph_single["gemm_ms"] else rf_gemm
 
     # FP64 tensor-pipe utilisation over the whole timed region (executed DMMA flops of every
     # solve / (time x GPUs x peak)); the Table-1 model figure is reported beside it
