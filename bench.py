@@ -12,7 +12,7 @@ paper's second method in the same run (its own throughput, latency and roofline)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 4096]
                   [--method chol|chol-svd] [--lanes L] [--no-cpu-baseline] [--no-e2e]
-                  [--no-chol-svd] [--v-gather]
+                  [--no-chol-svd] [--no-v-gather]
 
 --gpus N without torchrun re-executes this file under torch.distributed.run (N ranks on
 127.0.0.1). `--stub` swaps the GPU solver for a deterministic CPU stand-in on gloo so the
@@ -404,7 +404,7 @@ def run_ours(args, d: Dist):
 
     # optional eigenvector gather of one step to rank 0 (timed separately)
     v_gather = None
-    if args.v_gather and world > 1:
+    if not args.no_v_gather and world > 1:
         recv = torch.empty((n, 2 * n), dtype=torch.complex128, device=dev) if rank == 0 else None
         d.barrier()
         torch.cuda.synchronize()
@@ -653,8 +653,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-chol-svd", action="store_true", help="skip the CHOL+SVD sub-block")
-    ap.add_argument("--v-gather", action="store_true",
-                    help="N>1: also time one step's eigenvector gather to rank 0")
+    ap.add_argument("--no-v-gather", action="store_true",
+                    help="N>1: skip the separately timed gather of one step's eigenvectors to rank 0")
     ap.add_argument("--lanes", type=int, default=4, help="matrices in flight per GPU")
     ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU test hook
     args = ap.parse_args()
