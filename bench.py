@@ -448,8 +448,8 @@ def run_ours(args, d: Dist):
 
     # ---- CHOL+SVD in the same run (the paper's second method; reference bench.cpp:155, 190-204)
     svd_block = None
-    if method == "chol" and not args.no_chol_svd:
-        ks = min(args.steps, 3)
+    if method == "chol" and not args.no_chol_svd and total // lanes >= 2:
+        ks = min(args.steps, 3, total // lanes - 1)  # items [lanes, lanes + ks lanes) exist
         run_items(bse.Method.CholSvd, 0, lanes)  # warm-up: workspaces of the SVD route
         torch.cuda.synchronize()
         d.barrier()
