@@ -5,6 +5,7 @@
 #include <cstdio>
 
 #include "bse/backend.hpp"
+#include "bse/eigen_adapter.hpp"  // empty without Eigen (the reference's Eigen interop when present)
 #include "bse/solvers.hpp"
 #include "bse/verify.hpp"
 
