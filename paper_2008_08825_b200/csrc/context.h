@@ -40,7 +40,7 @@ struct bse_ctx {
   bse_ctx* twin[7]{};
   // look-ahead streams / events of the two concurrent Cholesky factorisations
   cudaStream_t la[2]{};
-  cudaEvent_t la_ev[4]{};
+  cudaEvent_t la_ev[8]{};  // 4 per concurrent Cholesky (zpotrf_lower's look-ahead)
 };
 
 namespace bseg {

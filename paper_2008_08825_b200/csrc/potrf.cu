@@ -1,7 +1,7 @@
 // potrf.cu — blocked right-looking Cholesky, lower (replaces LAPACKE_zpotrf 'L' at
 // proj/src/backend.cpp:51 and its NotPositiveDefinite pivot report, backend.cpp:52-56).
 //
-// Per nb = 64 block column j, two launches:
+// Per nb = 64 block column j (panels grouped three at a time, see zpotrf_lower):
 //   1. zpotrf_panel_kernel: every CTA factors the nb x nb diagonal block in shared memory,
 //      CTA 0 writes it back and reports the first non-positive / NaN pivot (LAPACK info),
 //      and each CTA solves its 32-row blocks of the panel A21 <- A21 L_jj^{-H} in place;
@@ -253,6 +253,76 @@ void zpotrf_lower(cudaStream_t s, int64_t n, z_t* A, int64_t lda, int* d_info, z
   // overlapping that panel). ev[0]: panel j done; ev[1]: the s2 update of step j-1 done.
   static const bool no_la = getenv("BSE_POTRF_NO_LA") != nullptr;  // A/B switch
   const bool la = s2 != nullptr && ev != nullptr && !no_la;
+  // panels per group (A/B switch BSE_POTRF_GROUP; 1 = the one-panel look-ahead below). n = 4096
+  // CHOL zpotrf: 5.48 ms with 1, 5.26 with 2, 5.25 with 3, 5.29 with 4, 5.70 with 6; the two
+  // concurrent factorisations of CHOL+SVD: 8.66, 8.18, 7.96, 8.04, 8.21 ms.
+  static const int group_env = getenv("BSE_POTRF_GROUP") ? atoi(getenv("BSE_POTRF_GROUP")) : 3;
+  const int G = std::max(1, std::min(group_env, 8));
+  if (la && G > 1) {
+    // Panels in groups of G (left-looking inside the group, right-looking across groups):
+    // block column a+q of the group first takes the group's panels a..a+q-1 in ONE rank-64q
+    // update, then is factored; after the group the trailing matrix takes ONE rank-64G
+    // update (k = 64G instead of G rank-64 updates: fewer C round trips per flop), split
+    // into the next group's first block column (s: the critical chain), its other G-1 block
+    // columns (s2 first, ev[1]) and the rest (s2, ev[2]). ev[0]: the group's panels done.
+    bool pend = false;
+    for (int64_t a0 = 0; a0 < n; a0 += int64_t(G) * kNB) {
+      bool done = false;
+      for (int q = 0; q < G && !done; ++q) {
+        const int64_t c = a0 + int64_t(q) * kNB;
+        if (c >= n) {
+          done = true;
+          break;
+        }
+        const int jbq = int(min64(kNB, n - c));
+        const int64_t restq = n - c - jbq;
+        if (q > 0) {  // the group's previous panels -> block column c (rows >= c)
+          if (q == 1 && pend) BSE_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
+          const z_t* P = A + c + a0 * lda;
+          zgemm(s, 0, 1, n - c, jbq, int(c - a0), mone, P, lda, P, lda, one, A + c + c * lda,
+                lda, kGeneral, kGeneral, 1, nullptr, 0);
+        }
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(restq, kPR))));
+        zpotrf_panel_kernel<<<grid, 256, smem, s>>>(A + c + c * lda, lda, jbq, c, restq, d_info,
+                                                    loaded);
+        BSE_LAUNCH_CHECK();
+        if (restq <= 0) done = true;
+      }
+      const int64_t r0 = a0 + int64_t(G) * kNB;  // first row / column after the group
+      if (done || r0 >= n) break;
+      BSE_CUDA(cudaEventRecord(ev[0], s));
+      const int kk = G * kNB;
+      const z_t* P = A + r0 + a0 * lda;  // rows >= r0 of the group's block columns
+      const int64_t rest = n - r0;
+      const int64_t w1 = min64(kNB, rest), w2 = min64(int64_t(G - 1) * kNB, rest - w1);
+      const int64_t n3 = rest - w1 - w2;
+      if (pend) BSE_CUDA(cudaStreamWaitEvent(s, ev[2], 0));
+      zgemm(s, 0, 1, rest, w1, kk, mone, P, lda, P, lda, one, A + r0 + r0 * lda, lda, kGeneral,
+            kGeneral, 1, nullptr, 0);
+      pend = false;
+      if (w2 > 0) {
+        BSE_CUDA(cudaStreamWaitEvent(s2, ev[0], 0));
+        const int64_t c2 = r0 + w1;
+        zgemm(s2, 0, 1, rest - w1, w2, kk, mone, P + w1, lda, P + w1, lda, one,
+              A + c2 + c2 * lda, lda, kGeneral, kGeneral, 1, nullptr, 0);
+        BSE_CUDA(cudaEventRecord(ev[1], s2));
+        if (n3 > 0) {
+          const int64_t c3 = c2 + w2;
+          zgemm(s2, 0, 1, n3, n3, kk, mone, P + w1 + w2, lda, P + w1 + w2, lda, one,
+                A + c3 + c3 * lda, lda, kGeneral, kGeneral, 1, nullptr, 0);
+        }
+        BSE_CUDA(cudaEventRecord(ev[2], s2));
+        pend = true;
+      }
+    }
+    if (pend) BSE_CUDA(cudaStreamWaitEvent(s, ev[2], 0));
+    if (zero_upper && n > 1) {
+      const int blocks = int(min64(ceil_div(n * n, 256), 148 * 32));
+      zero_strict_upper_kernel<<<blocks, 256, 0, s>>>(n, A, lda);
+      BSE_LAUNCH_CHECK();
+    }
+    return;
+  }
   bool big_pending = false;
   for (int64_t j = 0; j < n; j += kNB) {
     const int jb = int(min64(kNB, n - j));

@@ -316,7 +316,7 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   zaddsub(s, n, A, lda, B, ldb, b0, b1, ld);
   fork(c);
   zpotrf_lower(c->aux, n, b0, ld, info + 0, ws_potrf2, false, c->la[0], c->la_ev);
-  zpotrf_lower(s, n, b1, ld, info + 1, ws_potrf, false, c->la[1], c->la_ev + 2);
+  zpotrf_lower(s, n, b1, ld, info + 1, ws_potrf, false, c->la[1], c->la_ev + 4);
   join(c);
   clk.mark();
   certify(c, n, b0, b1, info);
