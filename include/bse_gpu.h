@@ -73,7 +73,7 @@ typedef struct bse_status {
 /* Per-phase device timings of the last solve (CUDA events on the context stream), ms. */
 typedef struct bse_phase_times {
   double product_pair;  /* M1=A+B, M2=A-B + Cholesky certificates                       */
-  double cholesky;      /* factor(s) kept for the method                                 */
+  double cholesky;      /* CHOL: the Cholesky factorisation of A-B alone (inside product_pair) */
   double triple;        /* CHOL: M = L^H M1 L ;  CHOL+SVD: C = L1^H L2                    */
   double reduce;        /* hetrd (CHOL) / gebrd (CHOL+SVD)                                */
   double tridiag;       /* tridiagonal divide & conquer                                   */

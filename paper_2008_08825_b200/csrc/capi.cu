@@ -252,6 +252,7 @@ int bse_ctx_create(bse_ctx** out, int device, bse_status* st) {
     BSE_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
     for (auto& ev : c->sink_ev) BSE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& ev : c->ev) BSE_CUDA(cudaEventCreate(&ev));
+    BSE_CUDA(cudaEventCreate(&c->chol_ev));
   } catch (const CudaError& ex) {
     delete c;
     return set_status(st, BSE_ERR_CUDA, ex.what());
@@ -293,6 +294,7 @@ int bse_ctx_destroy(bse_ctx* c) {
     }
   for (auto& ev : c->la_ev)
     if (ev) cudaEventDestroy(ev);
+  if (c->chol_ev) cudaEventDestroy(c->chol_ev);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->stream) cudaStreamDestroy(c->stream);

@@ -40,7 +40,8 @@ struct bse_ctx {
   bse_ctx* twin[7]{};
   // look-ahead streams / events of the two concurrent Cholesky factorisations
   cudaStream_t la[2]{};
-  cudaEvent_t la_ev[8]{};  // 4 per concurrent Cholesky (zpotrf_lower's look-ahead)
+  cudaEvent_t la_ev[8]{};
+  cudaEvent_t chol_ev = nullptr;  // start of the CHOL factorisation (bse_phase_times.cholesky)  // 4 per concurrent Cholesky (zpotrf_lower's look-ahead)
 };
 
 namespace bseg {
