@@ -233,6 +233,24 @@ __device__ __forceinline__ z_t zsum_strided16(const z_t* p, int64_t es, int star
   return zadd(zadd(s[0], s[1]), zadd(s[2], s[3]));
 }
 
+// The same sum with loads issued 8 at a time (for call sites short of registers: a batch of 16
+// that does not fit is serialised by the compiler into 16 round trips).
+__device__ __forceinline__ z_t zsum_strided8(const z_t* p, int64_t es, int start, int hi,
+                                             int stride) {
+  z_t s[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) s[u] = make_double2(0.0, 0.0);
+  for (int k0 = start; k0 < hi; k0 += 8 * stride) {
+    z_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = (k0 + u * stride < hi) ? p[int64_t(k0 + u * stride) * es] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u & 3] = zadd(s[u & 3], v[u]);
+  }
+  return zadd(zadd(s[0], s[1]), zadd(s[2], s[3]));
+}
+
 // Sums each of 16 complex values over the 32 lanes of a warp by recursive halving (16
 // complex shuffles in all); on return lane l holds the total of value (l >> 1).
 __device__ __forceinline__ z_t warp_transpose_zsum16(z_t (&v)[16]) {

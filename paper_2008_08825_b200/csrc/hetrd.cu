@@ -107,12 +107,19 @@ constexpr int kRing = 3;
 constexpr int kTabMax = 1280;  // per-CTA tile list capacity (n <= ~40k; checked on the host)
 using Ring = TileRing<kRing>;
 
-// Lower tile t (row-major over the triangle: (0,0), (1,0), (1,1), (2,0), ...) -> (bi, bj).
-__device__ __forceinline__ void tri_coords(int64_t t, int& bi, int& bj) {
-  bi = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-  while (int64_t(bi + 1) * (bi + 2) / 2 <= t) ++bi;
-  while (int64_t(bi) * (bi + 1) / 2 > t) --bi;
-  bj = int(t - int64_t(bi) * (bi + 1) / 2);
+// Tile t of a K x K lower tile triangle in "folded" column order: tile columns paired as
+// (0, K-1), (1, K-2), ... (K + 1 tiles per pair, the longest column with the shortest), each
+// column walked down from its diagonal tile. Contiguous runs of this order carry nearly the
+// same number of diagonal tiles and column ends, whose extra work balances across the CTAs.
+__device__ __forceinline__ void folded_coords(int t, int K, int& bi, int& bj) {
+  const int P = t / (K + 1), r = t - P * (K + 1);
+  if (r < K - P) {
+    bj = P;
+    bi = P + r;
+  } else {
+    bj = K - 1 - P;
+    bi = bj + (r - (K - P));
+  }
 }
 
 // One cooperative launch per nb-column panel. Per column g (index i in the panel):
@@ -157,11 +164,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // panel tile list: lower tiles of slabs [sp, nch) (a panel never straddles a 64-slab)
   const int sp = int((a.p0 + 1) / kT), K = a.nch - sp;
+  // Tiles in folded column order, one contiguous run per CTA (the remainder to the first CTAs,
+  // so the last CTA -- which also forms t1/t2 -- has the fewest): a run is a few segments
+  // (consecutive tiles of one tile column), whose column sums stay in registers (see the sweep).
   const int ntiles = K * (K + 1) / 2;
-  const int T = ntiles > cta ? (ntiles - cta + G - 1) / G : 0;
+  const int tq = ntiles / G, tr = ntiles % G;
+  const int t0 = cta * tq + min(cta, tr);
+  const int T = tq + (cta < tr ? 1 : 0);
   for (int k = tid; k < T; k += kThreads) {
     int bi, bj;
-    tri_coords(cta + int64_t(k) * G, bi, bj);
+    folded_coords(t0 + k, K, bi, bj);
     ttab[k] = bi | (bj << 16);
   }
   Ring ring;
@@ -248,20 +260,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     // Sweep: warp w owns tile columns 8w..8w+7, lane l rows l and l+32. Each element is read
-    // once for both products: row outputs reduce across warps (rowred, summed by warps 0-1
-    // after the barrier), column outputs within the warp (transpose reduction).
+    // once for both products. Row outputs (A_t v_C) reduce across warps per tile (rowred,
+    // summed by warps 0-3 after the tile's barrier, one double each). Column outputs
+    // (A_t^H v_R) stay in per-lane registers over a segment -- the CTA's consecutive tiles of
+    // one tile column, which share v_C -- and are reduced within the warp (transpose
+    // reduction) once, at the segment's last tile. Y slots: the row part of tile (I, J) goes
+    // to Y[I][J]; the column part of a whole segment to Y[J][I_last], the other tiles of the
+    // segment write zeros to their Y[J][I] (a diagonal tile's two slots coincide; every slot
+    // of a segment is >= J, so phase B, which sums the slots >= the current column, sees it).
     double vav = 0.0;
+    // (initialised: with undefined entry values ptxas keeps them live through phase B, which
+    // then serialises its batched partial-sum loads for want of registers)
+    z_t pc[8], vcc[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) pc[cc] = vcc[cc] = zero;
     for (int j = 0; j < T; ++j) {
       const int k = fwd ? j : T - 1 - j;
       const int bi = ttab[k] & 0xffff, bj = ttab[k] >> 16;
       const bool diag = (bi == bj);
+      const bool seg_start = j == 0 || (ttab[fwd ? k - 1 : k + 1] >> 16) != bj;
+      const bool seg_end = j == T - 1 || (ttab[fwd ? k + 1 : k - 1] >> 16) != bj;
       ring.acquire(k % kRing);
       const z_t* vr = vbuf + (j & 1) * 2 * kT;  // v over tile rows
       const z_t* vc = vr + kT;                  // v over tile cols
-      z_t vrv = zero, vcv = zero;               // this row's entries, for v^H A v below
-      if (tid < kT) {
-        vrv = vr[tid];
-        vcv = vc[tid];
+      // reducing threads (tid < 128: row tid / 2, component tid % 2): their v entries, read
+      // before the barrier (the buffer is refilled two tiles later)
+      double vrd = 0.0, vcd = 0.0;
+      if (tid < 2 * kT) {
+        vrd = reinterpret_cast<const double*>(vr)[tid];
+        vcd = reinterpret_cast<const double*>(vc)[tid];
+      }
+      if (seg_start) {
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          vcc[cc] = vc[8 * warp + cc];
+          pc[cc] = zero;
+        }
       }
       if (vthr && j + 1 < T) {  // next tile's vectors into the other buffer
         put_v(fwd ? j + 1 : T - 2 - j, raw, vbuf + ((j + 1) & 1) * 2 * kT);
@@ -269,17 +303,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const z_t* tl = ring.slot(k % kRing);
       const z_t v0 = vr[lane], v1 = vr[lane + 32];
-      z_t r0 = zero, r1 = zero, pc[8];
+      z_t r0 = zero, r1 = zero, r0b = zero, r1b = zero;  // two chains per row output
       if (!diag) {  // (CTA-uniform branch) the bulk of the sweep: no masks
         const z_t* tw = tl + ring_idx(lane, 8 * warp);
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
+        for (int cc = 0; cc < 8; cc += 2) {
           const z_t a0 = tw[cc * kRingT], a1 = tw[cc * kRingT + 32];
-          const z_t vcc = vc[8 * warp + cc];
-          zfma(r0, a0, vcc);
-          zfma(r1, a1, vcc);
-          pc[cc] = zcmul(a0, v0);
+          const z_t b0 = tw[(cc + 1) * kRingT], b1 = tw[(cc + 1) * kRingT + 32];
+          zfma(r0, a0, vcc[cc]);
+          zfma(r1, a1, vcc[cc]);
+          zfma(r0b, b0, vcc[cc + 1]);
+          zfma(r1b, b1, vcc[cc + 1]);
+          zcfma(pc[cc], a0, v0);
+          zcfma(pc[cc + 1], b0, v0);
           zcfma(pc[cc], a1, v1);
+          zcfma(pc[cc + 1], b1, v1);
         }
       } else {
 #pragma unroll
@@ -291,19 +329,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const z_t ac0 = low0 ? a0 : zero, ac1 = low1 ? a1 : zero;
           const z_t ar0 = low0 ? a0 : (lane == c ? make_double2(a0.x, 0.0) : zero);
           const z_t ar1 = low1 ? a1 : (lane + 32 == c ? make_double2(a1.x, 0.0) : zero);
-          const z_t vcc = vc[c];
-          zfma(r0, ar0, vcc);
-          zfma(r1, ar1, vcc);
-          pc[cc] = zero;
+          zfma(r0, ar0, vcc[cc]);
+          zfma(r1, ar1, vcc[cc]);
           zcfma(pc[cc], ac0, v0);
           zcfma(pc[cc], ac1, v1);
         }
       }
-      const z_t ctot = warp_transpose_zsum8(pc);
       z_t* rowred = swp + (j & 1) * (8 * kT + kT);  // [8 warps][64 rows] | [64 cols]
-      if ((lane & 3) == 0) rowred[8 * kT + 8 * warp + (lane >> 2)] = ctot;
-      rowred[warp * kT + lane] = r0;
-      rowred[warp * kT + lane + 32] = r1;
+      rowred[warp * kT + lane] = zadd(r0, r0b);
+      rowred[warp * kT + lane + 32] = zadd(r1, r1b);
+      if (seg_end) {  // CTA-uniform
+        const z_t ctot = warp_transpose_zsum8(pc);
+        if ((lane & 3) == 0) rowred[8 * kT + 8 * warp + (lane >> 2)] = ctot;
+      }
       __syncthreads();  // tile k fully read; this tile's partials and the next vectors visible
       {
         const int kn = fwd ? k + kRing : k - kRing;  // refill the slot with the tile it serves next
@@ -311,20 +349,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           ring.issue(k % kRing, &a.tmap, int64_t(sp + (ttab[kn] & 0xffff)) * kT,
                      int64_t(sp + (ttab[kn] >> 16)) * kT);
       }
-      if (tid < kT) {
-        z_t sr = rowred[tid];
+      if (tid < 2 * kT) {
+        const double* rd = reinterpret_cast<const double*>(rowred);
+        double sr = rd[tid];
 #pragma unroll
-        for (int w = 1; w < 8; ++w) sr = zadd(sr, rowred[w * kT + tid]);
-        const z_t sc = rowred[8 * kT + tid];
+        for (int w = 1; w < 8; ++w) sr += rd[w * 2 * kT + tid];
+        const double sc = seg_end ? rd[16 * kT + tid] : 0.0;
         const int gi = sp + bi, gj = sp + bj;
+        double* Yd = reinterpret_cast<double*>(a.Y);
         if (diag) {
-          a.Y[(int64_t(gi) * a.nch + gi) * kT + tid] = zadd(sr, sc);
+          Yd[(int64_t(gi) * a.nch + gi) * 2 * kT + tid] = sr + sc;
         } else {
-          a.Y[(int64_t(gi) * a.nch + gj) * kT + tid] = sr;
-          a.Y[(int64_t(gj) * a.nch + gi) * kT + tid] = sc;
+          Yd[(int64_t(gi) * a.nch + gj) * 2 * kT + tid] = sr;
+          Yd[(int64_t(gj) * a.nch + gi) * 2 * kT + tid] = sc;
         }
-        // v^H (A v) contributions of this tile: rows R (A_t v_C) and, mirrored, cols C
-        vav += zcmul(vrv, sr).x + zcmul(vcv, sc).x;
+        // v^H (A v) contributions: rows R (A_t v_C) and, mirrored, the segment's cols C
+        vav += vrd * sr + vcd * sc;
       }
     }
     {
