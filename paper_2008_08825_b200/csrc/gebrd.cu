@@ -120,9 +120,9 @@ __device__ __forceinline__ void gb_tsum(const z_t* partial, int stride, int off,
                           : make_double2(0.0, 0.0);
 }
 
-// Tile k of this CTA in the panel's K x K tile grid starting at slab sp.
-__device__ __forceinline__ void gb_tile_coords(int k, int K, int sp, int& rc, int& cc) {
-  const int t = int(blockIdx.x) + k * int(gridDim.x);
+// Tile t of the panel's K x K tile grid starting at slab sp, column-major: each CTA owns a
+// contiguous run (so consecutive tiles of a run mostly share their tile column).
+__device__ __forceinline__ void gb_tile_coords(int t, int K, int sp, int& rc, int& cc) {
   rc = sp + t % K;
   cc = sp + t / K;
 }
@@ -136,9 +136,13 @@ using Ring = TileRing<kRing>;
 // zero vector entry or produces a partial nobody reads (see the phase comments). Forward
 // sweeps end with tiles T-kRing..T-1 resident, backward sweeps with 0..kRing-1: each sweep
 // starts on the tiles the previous one ended on, and refills run kRing-1 tiles ahead.
-// Mapping: warp w owns tile columns 8w..8w+7, lane l rows l and l+32; column sums reduce
-// inside the warp (transpose reduction), row sums across warps through rowred (double
-// buffered, summed by warps 0-1 after the per-tile barrier). One CTA barrier per tile.
+// Mapping: warp w owns tile columns 8w..8w+7, lane l rows l and l+32; row sums reduce across
+// warps through rowred (double buffered, summed by warps 0-1 after the per-tile barrier), one
+// CTA barrier per tile. Column sums (P2, a forward sweep) stay in per-lane registers over a
+// segment -- consecutive tiles of one tile column -- and are reduced inside the warp
+// (transpose reduction) at the segment's last tile, which has its largest tile row: that
+// slot of P gets the segment's sum, the segment's other slots zeros (P3 sums the slots from
+// the current row slab on, and only rows >= g carry nonzero vector entries).
 template <bool kCols>
 __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const int* ttab,
                                          z_t* vbuf, z_t* swp, int T, bool forward, int64_t g,
@@ -169,6 +173,9 @@ __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const i
     if (T > 1) raw = fetch(forward ? 1 : T - 2);
   }
   __syncthreads();
+  z_t pc[8];
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) pc[c8] = zero;
   for (int j = 0; j < T; ++j) {
     const int k = forward ? j : T - 1 - j;
     const int rc = ttab[k] & 0xffff, cc = ttab[k] >> 16;
@@ -182,16 +189,22 @@ __device__ __forceinline__ void gb_sweep(const GebrdArgs& a, Ring& ring, const i
     z_t* rowred = swp + (j & 1) * 8 * kT;
     if (kCols) {
       const z_t v0 = vv[lane], v1 = vv[lane + 32];
-      z_t pc[8];
+      const bool seg_end = j == T - 1 || (ttab[forward ? k + 1 : k - 1] >> 16) != cc;
+      const z_t* tw = tl + ring_idx(lane, 8 * warp);
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
-        const int c = 8 * warp + c8;
-        pc[c8] = zero;
-        zcfma(pc[c8], tl[ring_idx(lane, c)], v0);
-        zcfma(pc[c8], tl[ring_idx(lane + 32, c)], v1);
+        zcfma(pc[c8], tw[c8 * kRingT], v0);
+        zcfma(pc[c8], tw[c8 * kRingT + 32], v1);
       }
-      const z_t tot = warp_transpose_zsum8(pc);
-      if ((lane & 3) == 0) a.P[(int64_t(cc) * a.nch + rc) * kT + 8 * warp + (lane >> 2)] = tot;
+      z_t* slot = a.P + (int64_t(cc) * a.nch + rc) * kT + 8 * warp + (lane >> 2);
+      if (seg_end) {  // CTA-uniform
+        const z_t tot = warp_transpose_zsum8(pc);
+        if ((lane & 3) == 0) *slot = tot;
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) pc[c8] = zero;
+      } else if ((lane & 3) == 0) {
+        *slot = zero;
+      }
     } else {
       z_t r0 = zero, r1 = zero;
 #pragma unroll
@@ -258,10 +271,12 @@ __global__ void __launch_bounds__(kThreads, 1) gebrd_panel_kernel(const __grid_c
   };
   // panel tile grid: slabs [sp, nch)^2 (a panel never straddles a 64-slab)
   const int sp = int(a.p0 / kT), K = a.nch - sp;
-  const int T = (K * K > cta) ? (K * K - cta + G - 1) / G : 0;
+  const int tq = K * K / G, tr = K * K % G;  // contiguous runs, the remainder to the first CTAs
+  const int t0 = cta * tq + min(cta, tr);
+  const int T = tq + (cta < tr ? 1 : 0);
   for (int k = tid; k < T; k += kThreads) {
     int rc, cc;
-    gb_tile_coords(k, K, sp, rc, cc);
+    gb_tile_coords(t0 + k, K, sp, rc, cc);
     ttab[k] = rc | (cc << 16);
   }
   ring.init(reinterpret_cast<z_t*>(sm_ring), bars);
