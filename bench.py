@@ -112,6 +112,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(k)
         return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_mhz_mean": round(statistics.mean(sm), 1) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(self.samples)}
 
@@ -542,7 +543,8 @@ def run_ours(args, d: Dist):
             return d.max(e0.elapsed_time(e1))
 
         batched(host[: args.warmup * lanes])  # untimed: staging buffers, lane contexts
-        ems = timed(lambda: batched(host[args.warmup * lanes: total]))
+        with ClockSampler(local) as eclk:  # the clocks of the e2e region too
+            ems = timed(lambda: batched(host[args.warmup * lanes: total]))
         for k in range(args.warmup):
             single(*host[k])
         ems1 = timed(lambda: [single(*host[args.warmup + k]) for k in range(args.steps)])
@@ -550,6 +552,7 @@ def run_ours(args, d: Dist):
                "unit": "TFLOP/s", "h2d_bytes_per_step": lanes * 2 * n * n * 16,
                "d2h_bytes_per_step": lanes * (2 * n * n * 16 + n * 8),
                "ms_per_step": ems / args.steps,
+               "clocks": eclk.summary(),
                "path": f"bse_solve_batched over the K x {lanes} timed matrices ({lanes} lanes; "
                        "pinned host buffers; each lane uploads its next item and downloads its "
                        "previous one while it solves)",
