@@ -460,3 +460,39 @@ def test_solve_batched_edge_cases():
         bse.solve_batched(bse.Method.Chol, [good, good, bad, bad, good], ctx=ctx)
     assert ei.value.index == 2 and len(ei.value.results) == 2
     ctx.close()
+
+
+@pytest.mark.parametrize("pad", [0, 3])
+def test_solve_batched_pinned_outputs_stream_same_bits(pad):
+    """bse_solve_batched into page-locked V buffers downloads each item with the L2-streaming
+    copy kernel (zcopy2d_to_host_streaming) instead of the copy engine; pageable outputs take
+    cudaMemcpy2DAsync. Same lanes, same solves: the outputs must be bit-identical, also with a
+    padded leading dimension (ldv = 2n + pad)."""
+    import ctypes
+
+    import torch
+
+    n, k = 300, 4
+    ctx = bse.Context(0)
+    ctx.set_batch_lanes(2)
+    hs = [bse.from_blocks(*configs.config2(40 + s, n=n)) for s in range(k)]
+    ref = bse.solve_batched(bse.Method.Chol, hs, ctx=ctx)
+    ldv = 2 * n + pad
+    hv = [torch.zeros((n, ldv), dtype=torch.complex128).pin_memory() for _ in range(k)]
+    hl = [torch.zeros(n, dtype=torch.float64).pin_memory() for _ in range(k)]
+    arr = lambda ptrs: (ctypes.c_void_p * k)(*ptrs)  # noqa: E731
+    ns = np.zeros((k, n), dtype=np.int64)
+    nn = np.zeros(k, dtype=np.int64)
+    failed = ctypes.c_int64(-1)
+    st = bse.Status()
+    rc = bse._lib.lib().bse_solve_batched(
+        ctx.handle, int(bse.Method.Chol), n, k, arr([h.a.ctypes.data for h in hs]), n,
+        arr([h.b.ctypes.data for h in hs]), n, arr([t.data_ptr() for t in hl]),
+        arr([t.data_ptr() for t in hv]), ldv, ns.ctypes.data_as(ctypes.c_void_p),
+        nn.ctypes.data_as(ctypes.c_void_p), ctypes.byref(failed), ctypes.byref(st))
+    assert rc == 0, st.message
+    for i in range(k):
+        v = hv[i].numpy()[:, : 2 * n].T  # column-major 2n x n with ld 2n + pad
+        assert np.array_equal(hl[i].numpy(), ref[i].lambda_)
+        assert np.array_equal(v, ref[i].v)
+    ctx.close()
