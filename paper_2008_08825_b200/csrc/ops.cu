@@ -22,7 +22,8 @@ __global__ void zaddsub_kernel(int64_t n, const z_t* __restrict__ A, int64_t lda
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e % n, j = e / n;
-    const z_t a = A[i + j * lda], b = B[i + j * ldb];
+    // the inputs are read once: streaming loads (evict-first in L2, see assemble_kernel)
+    const z_t a = __ldcs(A + i + j * lda), b = __ldcs(B + i + j * ldb);
     if (M1) M1[i + j * ldm] = zadd(a, b);
     if (M2) M2[i + j * ldm] = zsub(a, b);
   }
@@ -40,7 +41,7 @@ __global__ void real_to_complex_kernel(int64_t rows, int64_t cols, const double*
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e % rows, j = e / rows;
-    out[i + j * ldo] = make_double2(Z[i + j * ldz], 0.0);
+    out[i + j * ldo] = make_double2(__ldcs(Z + i + j * ldz), 0.0);
   }
 }
 
@@ -152,7 +153,10 @@ __global__ void assemble_kernel(int64_t n, int64_t k, const z_t* __restrict__ V1
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e % n, j = e / n;
-    const z_t a = V1[i + j * ld1], b = V2[i + j * ld2];
+    // last use of V1 / V2 and the solve's output V (n x 2n: 512 MB at n = 4096): streaming
+    // loads and stores, so they leave L2 first and the concurrent batch lanes keep their
+    // working sets (a copy-engine D2H of V slowed the lanes by 5 % through L2 eviction)
+    const z_t a = __ldcs(V1 + i + j * ld1), b = __ldcs(V2 + i + j * ld2);
     z_t x, y;
     if (dsq && !(dsq[j] > 0.0)) {
       const double mag = fmax(sqrt(fabs(dsq[j])), *floor_p);
@@ -168,8 +172,8 @@ __global__ void assemble_kernel(int64_t n, int64_t k, const z_t* __restrict__ V1
       x = zscale(a, s1);
       y = zscale(b, s2);
     }
-    V[i + j * ldv] = zscale(zadd(x, y), 0.5);
-    V[(n + i) + j * ldv] = zscale(zsub(y, x), 0.5);
+    __stcs(V + i + j * ldv, zscale(zadd(x, y), 0.5));
+    __stcs(V + (n + i) + j * ldv, zscale(zsub(y, x), 0.5));
   }
 }
 
