@@ -142,7 +142,10 @@ int bse_solve_device(bse_ctx* ctx, int method, int64_t n,
 /* Batch driver: solves `batch` independent matrices with the same
  * method and shape from host buffers a[i], b[i] into lambda[i], v[i]. The upload of matrix
  * i+1 and the download of matrix i-1 run on copy streams while matrix i computes, so with
- * page-locked host buffers the PCIe traffic hides behind the solves. Items run on
+ * page-locked host buffers the PCIe traffic hides behind the solves. A page-locked v[i] is
+ * written by a small streaming-copy kernel (evict-first loads, stores straight over PCIe)
+ * rather than the copy engine, whose 512 MB-per-item reads pass through L2 and evict the
+ * other solves' working sets; pageable outputs take cudaMemcpy. Items run on
  * bse_ctx_set_batch_lanes() lanes (default 4 solves in flight, item i on lane i % lanes).
  *   near_singular  : null or capacity batch*n (row i holds matrix i's flagged indices)
  *   n_near_singular: null or capacity batch
