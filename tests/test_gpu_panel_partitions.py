@@ -60,3 +60,55 @@ def test_panels_under_cta_counts(ctas, n):
     assert e2 <= 1e-11, e2
     assert r1 <= tol, r1
     assert r2 <= tol, r2
+
+
+SPECIAL = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2008_08825_b200 as bse
+n, kind = {n}, {kind!r}
+rng = np.random.default_rng(7)
+q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+if kind == "repeated":      # three eigenvalues with multiplicities n/2, n/4, n/4
+    lam = np.repeat([1.0, -2.0, 5.0], [n // 2, n // 4, n - n // 2 - n // 4])
+    h = (q * lam) @ q.conj().T
+elif kind == "diagonal":    # every reflector is the identity (tau = 0)
+    h = np.diag(rng.standard_normal(n)).astype(complex)
+elif kind == "tridiagonal":  # already reduced: x = 0 below the subdiagonal in every column
+    h = np.diag(rng.standard_normal(n)).astype(complex)
+    off = rng.standard_normal(n - 1) + 1j * rng.standard_normal(n - 1)
+    h += np.diag(off, -1) + np.diag(off.conj(), 1)
+elif kind == "graded":      # entries from 1 down to 1e-12 across the matrix
+    s = np.logspace(0, -6, n)
+    x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (s[:, None] * (x + x.conj().T)) * s[None, :]
+h = np.asfortranarray((h + h.conj().T) / 2)
+he = bse.hermitian_eig(h.copy())
+w, v = he.values, he.vectors
+ref = np.linalg.eigvalsh(h)
+e = np.max(np.abs(np.sort(w) - ref)) / np.max(np.abs(ref))
+r = np.linalg.norm(h - (v * w) @ v.conj().T) / np.linalg.norm(h)
+o = np.linalg.norm(v.conj().T @ v - np.eye(n))
+print(e, r, o, 100 * n * np.finfo(float).eps)
+"""
+
+
+@pytest.mark.parametrize("kind", ["repeated", "diagonal", "tridiagonal", "graded"])
+@pytest.mark.parametrize("ctas", [0, 37])
+@pytest.mark.parametrize("n", [300, 1100])
+def test_hermitian_eig_special_structure(kind, ctas, n):
+    """Degenerate spectra (D&C deflation), reflectors with tau = 0 (diagonal input), input
+    already tridiagonal, and graded entries, through the restructured hetrd sweep at every SM
+    and at a lane's 37 CTAs, against numpy: eigenvalues 1e-12 of the largest, reconstruction
+    and orthogonality <= 100 n eps."""
+    env = dict(os.environ)
+    if ctas:
+        env["BSE_SOLO_PANEL_CTAS"] = str(ctas)
+    out = subprocess.run([sys.executable, "-c", SPECIAL.format(root=ROOT, n=n, kind=kind)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    e, r, o, tol = map(float, out.stdout.split()[-4:])
+    assert e <= 1e-12, e
+    assert r <= tol, r
+    assert o <= tol, o
