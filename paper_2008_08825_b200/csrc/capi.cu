@@ -961,6 +961,7 @@ int bse_svd(bse_ctx* c, int64_t n, const double* m, int64_t ldm, double* u, int6
     tgk_build(sm, n, d, e, td, te);
     dstedc(sm, m2, td, te, X, ws_st, info, n);  // only the positive half of the vectors
     tgk_extract(sm, n, X, dU, n, dV, n);
+    tgk_reorthogonalize(sm, n, td + n, dU, dV, n, reinterpret_cast<z_t*>(X), info + 1);
     zunmbr_q(sm, n, dM, n, tq, dU, n, n, ws_um);
     zunmbr_p(sm, n, dM, n, tp, dV, n, n, ws_um);
     // reference convention: s descending, u/v columns to match (backend.cpp:74-84)

@@ -5,6 +5,7 @@
 //   real D&C eigenvectors -> complex, TGK vector extraction for the SVD route.
 #include <cfloat>
 
+#include "blas.h"
 #include "ops.h"
 
 namespace bseg {
@@ -500,6 +501,122 @@ void herm_lower_sum(cudaStream_t s, int64_t n, const z_t* X, int64_t ldx, z_t* M
   const int64_t nt = (n + 31) / 32;
   herm_lower_sum_kernel<<<unsigned(nt * (nt + 1) / 2), 256, 0, s>>>(n, X, ldx, M, ldm);
   BSE_LAUNCH_CHECK();
+}
+
+
+// ------------------------------------------------------------ TGK vectors: small-sigma block
+__global__ void count_small_sigma_kernel(int64_t n, const double* __restrict__ sasc,
+                                         double tau, int* k) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const double lim = tau * sasc[n - 1];
+  int64_t c = 0;  // sasc ascending: the first index with sigma >= lim
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sasc[mid] < lim) lo = mid + 1;
+    else hi = mid;
+  }
+  c = lo;
+  *k = int(c);
+}
+
+__device__ __forceinline__ z_t block_zsum(z_t v, double* red) {  // red: 16 doubles
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  v = warp_zsum(v);
+  __syncthreads();
+  if (lane == 0) {
+    red[2 * wid] = v.x;
+    red[2 * wid + 1] = v.y;
+  }
+  __syncthreads();
+  z_t s = make_double2(0.0, 0.0);
+  for (int w = 0; w < nw; ++w) s = zadd(s, make_double2(red[2 * w], red[2 * w + 1]));
+  return s;
+}
+
+// One CTA: the b columns of X (n x b; unit length on entry to the first pass) from the last to
+// the first, each against the later ones of the block (modified Gram-Schmidt, two sweeps),
+// then normalised; with `replace`, a column left with less than half of its length is first
+// overwritten by a fixed pseudo-random vector.
+__global__ void __launch_bounds__(256) block_mgs_kernel(int64_t n, int b, z_t* X, int64_t ld,
+                                                        int replace, int64_t col0) {
+  __shared__ double red[16];
+  for (int jj = b - 1; jj >= 0; --jj) {
+    z_t* xj = X + int64_t(jj) * ld;
+    for (int sweep = 0; sweep < 2; ++sweep)
+      for (int i = jj + 1; i < b; ++i) {
+        const z_t* xi = X + int64_t(i) * ld;
+        z_t d = make_double2(0.0, 0.0);
+        for (int64_t r = threadIdx.x; r < n; r += blockDim.x) zcfma(d, xi[r], xj[r]);
+        d = block_zsum(d, red);
+        for (int64_t r = threadIdx.x; r < n; r += blockDim.x) xj[r] = zsub(xj[r], zmul(d, xi[r]));
+      }
+    double n1 = 0.0;
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) n1 += zabs2(xj[r]);
+    n1 = block_sum(n1, red);
+    // the extracted columns have unit length: one that kept less than half of it through the
+    // projections (here and the caller's against the later columns) is a combination of them
+    if (replace && !(n1 >= 0.25)) {
+      // collapsed onto later columns: a fixed pseudo-random direction (re-projected by the
+      // caller's next pass against the columns after the block, and by this kernel again)
+      for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+        // (seeded by the global column index: every replaced column gets its own direction)
+        uint64_t h = uint64_t(r) * 0x9E3779B97F4A7C15ull ^
+                     ((uint64_t(col0 + jj) + 1) * 0x632BE59BD9B4E019ull);
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        xj[r] = make_double2(double(int64_t(h >> 11) - (int64_t(1) << 52)) * 0x1.0p-52, 0.0);
+      }
+      n1 = 0.0;
+      for (int64_t r = threadIdx.x; r < n; r += blockDim.x) n1 += zabs2(xj[r]);
+      n1 = block_sum(n1, red);
+      for (int sweep = 0; sweep < 2; ++sweep)
+        for (int i = jj + 1; i < b; ++i) {
+          const z_t* xi = X + int64_t(i) * ld;
+          z_t d = make_double2(0.0, 0.0);
+          for (int64_t r = threadIdx.x; r < n; r += blockDim.x) zcfma(d, xi[r], xj[r]);
+          d = block_zsum(d, red);
+          for (int64_t r = threadIdx.x; r < n; r += blockDim.x) xj[r] = zsub(xj[r], zmul(d, xi[r]));
+        }
+      n1 = 0.0;
+      for (int64_t r = threadIdx.x; r < n; r += blockDim.x) n1 += zabs2(xj[r]);
+      n1 = block_sum(n1, red);
+    }
+    const double sc = n1 > 0.0 ? 1.0 / sqrt(n1) : 0.0;
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) xj[r] = zscale(xj[r], sc);
+  }
+}
+
+void tgk_reorthogonalize(cudaStream_t s, int64_t n, const double* sasc, z_t* Ub, z_t* Vb,
+                         int64_t ld, z_t* ws, int* kcount) {
+  if (n <= 1) return;
+  constexpr double kTau = 1e-3;  // below tau sigma_max the +-sigma mirror gap 2 sigma can
+                                 // cost a TGK vector its accuracy (error ~ eps ||B|| / sigma)
+  constexpr int kB = 32;
+  count_small_sigma_kernel<<<1, 32, 0, s>>>(n, sasc, kTau, kcount);
+  BSE_LAUNCH_CHECK();
+  int k = 0;
+  BSE_CUDA(cudaMemcpyAsync(&k, kcount, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BSE_CUDA(cudaStreamSynchronize(s));
+  if (k <= 0) return;
+  const z_t one = {1.0, 0.0}, zero = {0.0, 0.0}, mone = {-1.0, 0.0};
+  for (z_t* X : {Ub, Vb}) {
+    for (int64_t top = k; top > 0; top -= kB) {  // block [j0, top), largest sigma first
+      const int64_t j0 = max64(0, top - kB), b = top - j0, above = n - top;
+      for (int rep = 0; rep < 2; ++rep) {
+        for (int t = 0; t < 2 && above > 0; ++t) {  // CGS2 against the final columns [top, n)
+          zgemm(s, 1, 0, above, b, n, one, X + top * ld, ld, X + j0 * ld, ld, zero, ws, above,
+                0, 0, 0, nullptr, 0);  // general shapes
+          zgemm(s, 0, 0, n, b, above, mone, X + top * ld, ld, ws, above, one, X + j0 * ld, ld,
+                0, 0, 0, nullptr, 0);  // general shapes
+        }
+        block_mgs_kernel<<<1, 256, 0, s>>>(n, int(b), X + j0 * ld, ld, rep == 0, j0);
+        BSE_LAUNCH_CHECK();
+      }
+    }
+  }
 }
 
 }  // namespace bseg

@@ -22,6 +22,16 @@ void tgk_build(cudaStream_t s, int64_t n, const double* d, const double* e, doub
                double* te);
 void tgk_extract(cudaStream_t s, int64_t n, const double* X, z_t* Ub, int64_t ldu, z_t* Vb,
                  int64_t ldv);
+// Re-orthonormalises the extracted bidiagonal singular vectors Ub, Vb (n x n, columns in
+// ascending-sigma order sasc) whose sigma is below 1e-3 sigma_max, from the largest of them
+// down, each against every column with a larger sigma (block CGS2 + in-block MGS; a column
+// that collapses onto later ones -- numerically zero sigma, where the TGK eigenvectors of +s
+// and -s mix -- is replaced by a pseudo-random direction and orthonormalised again). The
+// change of such a column is of the size of its error, so sigma_j |du_j| stays at the
+// eps ||B|| level (backward stable). ws: n * 32 complex; kcount: one device int. Syncs the
+// stream once (to size the work); no further work when no sigma is that small.
+void tgk_reorthogonalize(cudaStream_t s, int64_t n, const double* sasc, z_t* Ub, z_t* Vb,
+                         int64_t ld, z_t* ws, int* kcount);
 // Relative-accuracy bisection refinement of ascending bidiagonal singular values (in place).
 // scratch: 2n + 2 doubles.
 void tgk_refine(cudaStream_t s, int64_t n, const double* d, const double* e, double* sig,

@@ -344,6 +344,9 @@ void solve_chol_svd_dev(bse_ctx* c, int64_t n, const z_t* A, int64_t lda, const 
   BSE_CUDA(cudaMemcpyAsync(sasc, td + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   tgk_refine(s, n, d, e, sasc, te);  // relative accuracy of the small singular values
   tgk_extract(s, n, X, b3, ld, b4, ld);
+  // numerically small singular values: orthonormal U_B / V_B columns (X is free after the
+  // extract; a no-op after one small count when every sigma >= 1e-3 sigma_max)
+  tgk_reorthogonalize(s, n, sasc, b3, b4, ld, reinterpret_cast<z_t*>(X), info + 3);
   fork(c);
   apply_prepared_reflectors(s, 1, n, n, b3, ld, n, ws_unmbr);             // U = Q U_B
   apply_prepared_reflectors(c->aux, 2, n, n - 1, b4, ld, n, ws_unmbr2);   // V = P V_B

@@ -112,3 +112,51 @@ def test_hermitian_eig_special_structure(kind, ctas, n):
     assert e <= 1e-12, e
     assert r <= tol, r
     assert o <= tol, o
+
+
+SPECIAL_SVD = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2008_08825_b200 as bse
+n, kind = {n}, {kind!r}
+rng = np.random.default_rng(11)
+x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+if kind == "diagonal":
+    g = np.diag(rng.standard_normal(n) + 1j * rng.standard_normal(n))
+elif kind == "bidiagonal":
+    g = np.diag(rng.standard_normal(n)).astype(complex) + np.diag(rng.standard_normal(n - 1), 1)
+elif kind == "rank_deficient":   # rank n/2: half of the singular values are zero
+    g = x[:, : n // 2] @ (rng.standard_normal((n // 2, n)) + 0j)
+elif kind == "graded":
+    s = np.logspace(0, -6, n)
+    g = s[:, None] * x
+g = np.asfortranarray(g)
+sv = bse.svd(g.copy())
+u, s, vh = sv.u, sv.s, sv.v.conj().T
+ref = np.linalg.svd(g, compute_uv=False)
+e = np.max(np.abs(np.sort(s)[::-1] - ref)) / ref[0]
+r = np.linalg.norm(g - (u * s) @ vh) / np.linalg.norm(g)
+ou = np.linalg.norm(u.conj().T @ u - np.eye(n))
+ov = np.linalg.norm(vh @ vh.conj().T - np.eye(n))
+print(e, r, ou, ov, 100 * n * np.finfo(float).eps)
+"""
+
+
+@pytest.mark.parametrize("kind", ["diagonal", "bidiagonal", "rank_deficient", "graded"])
+@pytest.mark.parametrize("ctas", [0, 37])
+@pytest.mark.parametrize("n", [300, 1100])
+def test_svd_special_structure(kind, ctas, n):
+    """The restructured gebrd sweeps (column segments) on diagonal, already-bidiagonal,
+    rank-deficient and graded inputs at every SM and at a lane's 37 CTAs, against numpy:
+    singular values 1e-12 of the largest, reconstruction and orthogonality <= 100 n eps."""
+    env = dict(os.environ)
+    if ctas:
+        env["BSE_SOLO_PANEL_CTAS"] = str(ctas)
+    out = subprocess.run([sys.executable, "-c", SPECIAL_SVD.format(root=ROOT, n=n, kind=kind)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    e, r, ou, ov, tol = map(float, out.stdout.split()[-5:])
+    assert e <= 1e-12, e
+    assert r <= tol, r
+    assert ou <= tol and ov <= tol, (ou, ov)
