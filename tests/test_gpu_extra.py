@@ -496,3 +496,23 @@ def test_solve_batched_pinned_outputs_stream_same_bits(pad):
         assert np.array_equal(hl[i].numpy(), ref[i].lambda_)
         assert np.array_equal(v, ref[i].v)
     ctx.close()
+
+
+@pytest.mark.parametrize("method", [bse.Method.Chol, bse.Method.CholSvd])
+@pytest.mark.parametrize("n", [96, 640])
+def test_degenerate_bse_spectrum(method, n):
+    """Physically degenerate excitations: A with eigenvalues of multiplicity n/4 and B = 0 (the
+    reference's decoupled case, test_solvers.cpp) and B a small multiple of A (commuting, the
+    multiplicities kept). lambda against the oracle's same method (1e-10), every eigenpair's
+    residual <= 100 n eps and Sigma-orthogonality <= 100 n eps (vectors inside a degenerate
+    eigenspace are not unique, so they are not compared)."""
+    q, _ = np.linalg.qr(crand(n, n))
+    ev = np.repeat([1.0, 2.0, 3.5, 7.0], n // 4)
+    a = (q * ev) @ q.conj().T
+    a = (a + a.conj().T) / 2
+    for b in (np.zeros_like(a), 0.25 * a):
+        r = bse.solve(method, bse.from_blocks(a, b))
+        ref, _, _ = oracle.solve("chol" if method == bse.Method.Chol else "chol-svd", a, b)
+        assert np.max(np.abs(r.lambda_ - ref) / ref) <= 1e-10
+        assert residual(a, b, r.lambda_, r.v).max() <= 100 * n * EPS
+        assert sigma_orthogonality_error(r.v) <= 100 * n * EPS

@@ -1,5 +1,5 @@
 """SVD orthogonality on ill-conditioned and rank-deficient inputs (dev tool): the TGK route
-with tgk_reorthogonalize against numpy-free checks of U^H U, V^H V and the reconstruction."""
+with tgk_reorthogonalize checked with numpy: U^H U, V^H V and the reconstruction."""
 import sys
 import numpy as np
 sys.path.insert(0, ".")
