@@ -160,3 +160,28 @@ def test_svd_special_structure(kind, ctas, n):
     assert e <= 1e-12, e
     assert r <= tol, r
     assert ou <= tol and ov <= tol, (ou, ov)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 129, 193, 517, 1031])
+def test_sizes_eig_svd_against_numpy(n):
+    """Tile-edge and odd sizes through the restructured panels (in-process, every SM):
+    eigenvalues / singular values 1e-12 of the largest, reconstructions and orthogonality
+    within 10 n eps (tools/size_fuzz.py: worst 2.4 n eps over 36 sizes up to 2100)."""
+    import paper_2008_08825_b200 as bse
+
+    rng = np.random.default_rng(n)
+    eps = np.finfo(float).eps
+    x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = np.asfortranarray(x + x.conj().T)
+    he = bse.hermitian_eig(h.copy())
+    ref = np.linalg.eigvalsh(h)
+    assert np.max(np.abs(np.sort(he.values) - ref)) <= 1e-12 * np.max(np.abs(ref))
+    q = he.vectors
+    assert np.linalg.norm(h - (q * he.values) @ q.conj().T) <= 10 * n * eps * np.linalg.norm(h)
+    assert np.linalg.norm(q.conj().T @ q - np.eye(n)) <= 10 * n * eps
+    sv = bse.svd(np.asfortranarray(x))
+    refs = np.linalg.svd(x, compute_uv=False)
+    assert np.max(np.abs(np.sort(sv.s)[::-1] - refs)) <= 1e-12 * refs[0]
+    assert np.linalg.norm(x - (sv.u * sv.s) @ sv.v.conj().T) <= 10 * n * eps * np.linalg.norm(x)
+    assert np.linalg.norm(sv.u.conj().T @ sv.u - np.eye(n)) <= 10 * n * eps
+    assert np.linalg.norm(sv.v.conj().T @ sv.v - np.eye(n)) <= 10 * n * eps
