@@ -362,6 +362,8 @@ bool zcopy2d_to_host_streaming(cudaStream_t s, int64_t rows, int64_t cols, const
     (void)cudaGetLastError();
     return false;
   }
+  // 16-byte vector accesses: an 8-byte-aligned complex buffer goes to the copy engine
+  if ((reinterpret_cast<uintptr_t>(dptr) | reinterpret_cast<uintptr_t>(src)) & 15u) return false;
   zcopy_d2h_stream_kernel<<<ctas, 256, 0, s>>>(rows, cols, src, lds, static_cast<z_t*>(dptr), ldd);
   BSE_LAUNCH_CHECK();
   return true;
