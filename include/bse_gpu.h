@@ -133,7 +133,8 @@ int bse_solve(bse_ctx* ctx, int method, int64_t n,
               int64_t* near_singular, int64_t* n_near_singular, bse_status* st);
 
 /* Same, device pointers (a, b, lambda, v on the context's device); near_singular stays a
- * host array. Synchronous at return. */
+ * host array. a, b and v must be 16-byte aligned (complex128 vectors; any cudaMalloc'd
+ * pointer is), else BSE_ERR_INVALID_SPEC. Synchronous at return. */
 int bse_solve_device(bse_ctx* ctx, int method, int64_t n,
                      const double* d_a, int64_t lda, const double* d_b, int64_t ldb,
                      double* d_lambda, double* d_v, int64_t ldv,

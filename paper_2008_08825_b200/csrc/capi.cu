@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <initializer_list>
 #include <thread>
 #include <cfloat>
 #include <cstring>
@@ -197,6 +198,14 @@ struct SinkScope {
   }
 };
 
+// Device operands are read and written as 16-byte complex vectors.
+void check_aligned16(std::initializer_list<const void*> ptrs) {
+  for (const void* p : ptrs)
+    if (reinterpret_cast<uintptr_t>(p) & 15u)
+      throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1,
+                        "device matrix pointers must be 16-byte aligned (complex128)"};
+}
+
 void check_dims(int64_t n, int64_t lda, int64_t ldb) {
   if (n < 1) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "blocks must be at least 1x1"};
   if (lda < n || ldb < n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "leading dimension too small"};
@@ -351,6 +360,7 @@ int bse_solve_device(bse_ctx* c, int method, int64_t n, const double* d_a, int64
   return guarded(c, st, [&] {
     check_dims(n, lda, ldb);
     if (ldv < 2 * n) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < 2n"};
+    check_aligned16({d_a, d_b, d_v});
     std::vector<int64_t> flagged;
     run_solve(c, method, n, reinterpret_cast<const z_t*>(d_a), lda,
               reinterpret_cast<const z_t*>(d_b), ldb, d_lambda, reinterpret_cast<z_t*>(d_v),
@@ -660,6 +670,7 @@ int bse_solve_batched_device(bse_ctx* c, int method, int64_t n, int64_t batch,
   if (failed_index) *failed_index = -1;
   return guarded(c, st, [&] {
     check_batch(n, lda, ldb, ldv, batch, d_a, d_b, d_lambda, d_v);
+    for (int64_t i = 0; i < batch; ++i) check_aligned16({d_a[i], d_b[i], d_v[i]});
     const BatchIO io{method, n, lda, ldb, ldv, d_a, d_b, d_lambda, d_v, near_singular,
                      n_near_singular, true};
     run_batch(c, io, batch, failed_index);

@@ -135,3 +135,23 @@ def test_indefinite_m1_reported_like_the_reference(strict):
         ctx.close()
     assert eg.value.which == bse.Block.M1 and eo.value.block == 0
     assert str(eg.value) == str(eo.value)
+
+
+def test_device_pointers_must_be_16_byte_aligned():
+    """bse_solve_device / bse_solve_batched_device read and write complex128 as 16-byte
+    vectors: an 8-byte-aligned device operand is rejected with InvalidSpec (no launch)."""
+    import torch
+
+    n = 64
+    a, b = configs.config2(5, n=n)
+    dev = torch.device("cuda", 0)
+    buf = torch.zeros(2 * n * n + 2, dtype=torch.float64, device=dev)
+    da = torch.from_numpy(a.T.copy()).to(dev)
+    lam = torch.empty(n, dtype=torch.float64, device=dev)
+    v = torch.empty((n, 2 * n), dtype=torch.complex128, device=dev)
+    with pytest.raises(bse.InvalidSpec):
+        bse.solve_device(bse.Method.Chol, n, da.data_ptr(), buf.data_ptr() + 8, lam.data_ptr(),
+                         v.data_ptr())
+    with pytest.raises(bse.InvalidSpec):
+        bse.solve_batched_device(bse.Method.Chol, n, [da.data_ptr()], [buf.data_ptr() + 8],
+                                 [lam.data_ptr()], [v.data_ptr()])
