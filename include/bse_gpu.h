@@ -14,7 +14,8 @@
  *
  * Host-pointer entry points copy host->device, run entirely on the GPU bound to the
  * context, and copy results back before returning (synchronous, like the reference).
- * The *_device variants take device pointers and enqueue on the context's stream.
+ * The *_device variants take device pointers and enqueue on the context's stream; their
+ * complex128 matrix operands must be 16-byte aligned (BSE_ERR_INVALID_SPEC otherwise).
  */
 #ifndef BSE_GPU_H
 #define BSE_GPU_H

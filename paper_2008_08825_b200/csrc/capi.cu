@@ -1022,6 +1022,7 @@ int bse_residual_device(bse_ctx* c, int64_t n, const double* d_a, int64_t lda,
                         const double* d_v, int64_t ldv, double* d_out, bse_status* st) {
   return guarded(c, st, [&] {
     check_residual_dims(n, lda, ldb, k, ldv);
+    check_aligned16({d_a, d_b, d_v});
     Bump w = arena(c, residual_workspace_bytes(n, k));
     residual_dev(c->stream, n, reinterpret_cast<const z_t*>(d_a), lda,
                  reinterpret_cast<const z_t*>(d_b), ldb, k, d_lambda,
@@ -1067,6 +1068,7 @@ int bse_sigma_orthogonality_error_device(bse_ctx* c, int64_t rows, int64_t k, co
   return guarded(c, st, [&] {
     const int64_t h = half_dimension(rows, "sigma_orthogonality_error");
     if (k < 0 || ldv < rows) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, "ldv < rows"};
+    check_aligned16({d_v});
     *out = 0.0;
     if (k == 0) return;
     Bump w = arena(c, sigma_orth_workspace_bytes(k) + 1024);
@@ -1112,6 +1114,7 @@ int bse_check_form_device(bse_ctx* c, int form, int64_t rows, const double* d_m,
     if (form != 1 && form != 2) throw DomainError{BSE_ERR_INVALID_SPEC, 0, -1, "form must be 1 or 2"};
     if (ldm < rows) throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1, std::string(who) + ": matrix must be square"};
     const int64_t h = half_dimension(rows, who);
+    check_aligned16({d_m});
     Bump w = arena(c, form_workspace_bytes() + 1024);
     double* d_out = w.take<double>(4);
     form_dev(c->stream, form, h, reinterpret_cast<const z_t*>(d_m), ldm, d_out, w);
@@ -1149,6 +1152,7 @@ int bse_negative_spectrum_device(bse_ctx* c, int64_t n, int64_t k, const double*
     if (n < 0 || k < 0 || ldv < 2 * n || ldvo < 2 * n)
       throw DomainError{BSE_ERR_DIMENSION_MISMATCH, 0, -1,
                         "spectral result does not match the matrix dimension"};
+    check_aligned16({d_v, d_v_out});
     negative_spectrum_dev(c->stream, n, k, d_lambda, reinterpret_cast<const z_t*>(d_v), ldv,
                           d_lambda_out, reinterpret_cast<z_t*>(d_v_out), ldvo);
     BSE_CUDA(cudaStreamSynchronize(c->stream));
