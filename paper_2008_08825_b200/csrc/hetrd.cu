@@ -9,9 +9,10 @@
 //    phases replace LAPACK's ~8 BLAS-2 calls (see hetrd_panel_kernel):
 //      A  reflector (zlarfg, recomputed redundantly by every CTA from per-slab partial
 //         norms) and the Hermitian matrix-vector product y = A22 v over the LOWER triangle
-//         only: 64x64 tiles (cp.async into shared memory), each contributing A_t v to its
-//         row chunk and A_t^H v to its column chunk (2.67 n^3 bytes over the reduction, the
-//         HBM-bound half of zhetrd), plus per-CTA partials of v^H A22 v;
+//         only: 64x64 tiles (TMA into a shared-memory ring, one contiguous run of the
+//         folded tile order per CTA), each contributing A_t v to its row chunk and A_t^H v
+//         to its column chunk (2.67 n^3 bytes over the reduction, the HBM-bound half of
+//         zhetrd), plus per-CTA partials of v^H A22 v;
 //      B  alpha from v^H A v (no extra dot reduction), W(:,g) = tau (y - V t1 - W t2) +
 //         alpha v, and the next column's update with its partial norms / V^H x / W^H x.
 //    All partial sums have a fixed order (bit-deterministic).
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_ring + sizeof(z_t) * kRing * kRingT * kRingT);
   z_t* vbuf = reinterpret_cast<z_t*>(bars + 2 * kRing);  // 2 x [v rows | v cols] of a tile
   int* ttab = reinterpret_cast<int*>(vbuf + 4 * kT);       // this CTA's tiles: bi | bj << 16
-  z_t* swp = reinterpret_cast<z_t*>(ttab + kTabMax);       // 2 x (8 x kT + kT): sweep partials
+  z_t* swp = reinterpret_cast<z_t*>(ttab + kTabMax);       // 2 x (8 x kT + kT): row partials | segment column sums
   z_t* wg = swp + 2 * (8 * kT + kT);       // NB : W(g+1, p)
   z_t* vg = wg + NB;                       // NB : V(g+1, p)
   z_t* xs = vg + NB;                       // kT : next column values of the slab
