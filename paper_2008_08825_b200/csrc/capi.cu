@@ -531,8 +531,11 @@ void run_lane(bse_ctx* c, const BatchIO& io, const std::vector<int64_t>& items, 
     BSE_CUDA(cudaStreamWaitEvent(c->copy, comp_done[k], 0));
     BSE_CUDA(cudaMemcpyAsync(io.lambda[i], dL[k], sizeof(double) * size_t(n),
                              cudaMemcpyDeviceToHost, c->copy));
-    if (!(is_pinned(io.v[i]) && zcopy2d_to_host_streaming(c->copy, 2 * n, n, dV[k], 2 * n,
-                                                          reinterpret_cast<z_t*>(io.v[i]), io.ldv)))
+    // the lane's last item has no later solve of its own to protect: the faster copy engine
+    const bool last = j + 1 == items.size();
+    if (last || !(is_pinned(io.v[i]) &&
+                  zcopy2d_to_host_streaming(c->copy, 2 * n, n, dV[k], 2 * n,
+                                            reinterpret_cast<z_t*>(io.v[i]), io.ldv)))
       BSE_CUDA(cudaMemcpy2DAsync(io.v[i], size_t(io.ldv) * sizeof(z_t), dV[k],
                                  size_t(2 * n) * sizeof(z_t), size_t(2 * n) * sizeof(z_t),
                                  size_t(n), cudaMemcpyDeviceToHost, c->copy));
