@@ -525,7 +525,7 @@ def test_solve_batched_pinned_outputs_misaligned():
 
     import torch
 
-    n, k = 200, 2
+    n, k = 200, 4  # two items per lane: the first goes through the streaming path's check
     ctx = bse.Context(0)
     ctx.set_batch_lanes(2)
     hs = [bse.from_blocks(*configs.config2(60 + s, n=n)) for s in range(k)]
